@@ -182,6 +182,25 @@ class CpuShooting:
                                            _p(sc), _p(g), *self._red(strategy, block, threads)))
         return sc[0], sc[1], sc[2], g
 
+    def pair_rows(self, prec, q, p, rows, sigma, alpha=None, beta=None, strategy="blocked_tree", block=256,
+                  threads=0):
+        """(hq, hp) -- or (d_alpha, d_beta) when alpha/beta are given -- for the listed rows only."""
+        assert self.prefix == "orc"
+        q, p = _arr(q), _arr(p)
+        n, d = q.shape
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        fn = self.lib.orc_pair_rows
+        fn.argtypes = [c_int, c_int, c_size_t, c_double, _dp, _dp, _dp, _dp, c_size_t, POINTER(c_size_t), _dp,
+                       c_int, c_size_t, c_uint]
+        fn.restype = c_int
+        sums = np.empty((rows.size, 2 * d))
+        a = _arr(alpha) if alpha is not None else None
+        b = _arr(beta) if beta is not None else None
+        self._check(fn(PREC[prec], d, n, sigma, _p(q), _p(p), _p(a) if a is not None else None,
+                       _p(b) if b is not None else None, rows.size, rows.ctypes.data_as(POINTER(c_size_t)), _p(sums),
+                       *self._red(strategy, block, threads)))
+        return sums[:, :d].copy(), sums[:, d:].copy()
+
     def velocities(self, prec, q, p, points, sigma, strategy="blocked_tree", block=256, threads=0):
         q, p, points = _arr(q), _arr(p), _arr(points)
         n, d = q.shape

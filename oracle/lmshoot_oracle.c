@@ -344,6 +344,32 @@ int orc_velocities(int prec, int dim, size_t n, size_t m, double sigma, const do
   return 0;
 }
 
+/* sums: nrows x 2*dim = (hq | hp) of derivatives, or (d_alpha | d_beta) of adjoint_step when alpha/beta
+ * are non-NULL, for the listed rows only. */
+int orc_pair_rows(int prec, int dim, size_t n, double sigma, const double* q, const double* p,
+                  const double* alpha, const double* beta, size_t nrows, const size_t* rows, double* sums,
+                  int strategy, size_t block, unsigned threads)
+{
+  int rc = check_args(dim, sigma, block);
+  if (rc) return rc;
+  for (size_t r = 0; r < nrows; ++r)
+    if (rows[r] >= n) return 1;
+  size_t nd = n * dim;
+  const int adjoint = alpha != NULL && beta != NULL;
+#define BODY(R, S)                                                                               \
+  {                                                                                              \
+    R *tq = load##S(q, nd), *tp = load##S(p, nd);                                                \
+    R *ta = adjoint ? load##S(alpha, nd) : NULL, *tb = adjoint ? load##S(beta, nd) : NULL;       \
+    R* out = (R*)malloc((nrows ? nrows : 1) * 2 * dim * sizeof(R));                              \
+    rows_T##S(adjoint, dim, n, sigma, tq, tp, ta, tb, nrows, rows, out, strategy, block, threads); \
+    store##S(out, nrows * 2 * dim, sums);                                                        \
+    free(tq); free(tp); free(ta); free(tb); free(out);                                           \
+  }
+  if (prec == 0) BODY(float, _f32) else BODY(double, _f64)
+#undef BODY
+  return 0;
+}
+
 /* flow.hpp:66-81: x += dt * v(x, t) for t = 0..T-1 with the trajectory's own dt = T(1/T). */
 int orc_warp_points(int prec, int dim, size_t n, size_t m, double sigma, int timesteps,
                     const double* traj_q, const double* traj_p, const double* points, double* out,

@@ -42,6 +42,12 @@ int orc_mismatch_sq(int prec, int dim, size_t n, const double* a, const double* 
 int orc_compute_gradient(int prec, int dim, size_t n, double sigma, double lambda, int timesteps,
                          const double* q0, const double* p0, const double* target, double* scalars,
                          double* grad, int strategy, size_t block, unsigned threads);
+/* Row subset of derivatives (alpha = beta = NULL: sums = hq|hp) or adjoint_step (sums = d_alpha|d_beta):
+ * identical terms and per-row reduction, only the listed rows; pinned against the full calls in
+ * tests/test_oracle.py. */
+int orc_pair_rows(int prec, int dim, size_t n, double sigma, const double* q, const double* p,
+                  const double* alpha, const double* beta, size_t nrows, const size_t* rows, double* sums,
+                  int strategy, size_t block, unsigned threads);
 int orc_velocities(int prec, int dim, size_t n, size_t m, double sigma, const double* q, const double* p,
                    const double* points, double* out, int strategy, size_t block, unsigned threads);
 int orc_warp_points(int prec, int dim, size_t n, size_t m, double sigma, int timesteps,

@@ -1,0 +1,18 @@
+"""lmshoot_b200: B200-native (sm_100a) objective-and-gradient hot path of landmark geodesic shooting
+(arXiv 1907.04839) behind the reference's own interface.  See DESIGN.md and include/lmshoot_b200.h.
+
+Importing this package does not touch the GPU; the C-ABI library is loaded on first use and its
+absence is an error (no CPU fallback)."""
+from .errors import CommError, CudaError, DivergedError, NumericalError, ShapeError, StateError  # noqa: F401
+from .lbfgs import LbfgsParams, MinimizeResult, minimize  # noqa: F401
+from .registration import RegistrationResult, register_landmarks  # noqa: F401
+from .shooting import (GradientResult, HamiltonianSystem, ShootingConfig, comm_unique_id, gaussian_kernel,  # noqa: F401
+                       kernel_scale)
+from .synth import make_synthetic_pair, make_template_points, rng_normals, rng_uniforms  # noqa: F401
+
+__all__ = [
+    "HamiltonianSystem", "ShootingConfig", "GradientResult", "LbfgsParams", "MinimizeResult", "minimize",
+    "register_landmarks", "RegistrationResult", "make_synthetic_pair", "make_template_points", "rng_normals",
+    "rng_uniforms", "gaussian_kernel", "kernel_scale", "comm_unique_id", "ShapeError", "DivergedError",
+    "NumericalError", "CudaError", "StateError", "CommError",
+]

@@ -1,0 +1,317 @@
+// extern "C" surface of liblmshoot_b200.so (include/lmshoot_b200.h).  Exceptions never cross it.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+#include <random>
+
+#include "system.cuh"
+
+struct lms_system {
+  lms::SystemBase* impl = nullptr;
+  int device = 0;
+};
+
+namespace {
+
+template <class Fn>
+int guarded(lms_system* sys, Fn&& fn)
+{
+  if (!sys || !sys->impl) return LMS_ERR_STATE;
+  lms::SystemBase* s = sys->impl;
+  s->last_diverged_step = -1;
+  s->last_diverged_point = -1;
+  s->last_message.clear();
+  try {
+    cudaError_t e = cudaSetDevice(sys->device);
+    if (e != cudaSuccess) throw lms::CudaFailure{e, "cudaSetDevice", __LINE__};
+    fn(s);
+    return LMS_OK;
+  } catch (const lms::StatusError& e) {
+    s->last_message = e.msg;
+    return e.code;
+  } catch (const lms::CudaFailure& e) {
+    s->last_message = std::string(cudaGetErrorString(e.err)) + " in " + e.what;
+    cudaGetLastError();
+    return LMS_ERR_CUDA;
+  } catch (const std::bad_alloc&) {
+    s->last_message = "host allocation failed";
+    return LMS_ERR_CUDA;
+  } catch (...) {
+    s->last_message = "unexpected exception";
+    return LMS_ERR_CUDA;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lms_status_string(int status)
+{
+  switch (status) {
+    case LMS_OK: return "ok";
+    case LMS_ERR_SHAPE: return "shape mismatch (lmshoot::ShapeError)";
+    case LMS_ERR_DIVERGED: return "non-finite state (lmshoot::DivergedError)";
+    case LMS_ERR_INVALID: return "invalid argument (std::invalid_argument)";
+    case LMS_ERR_NUMERICAL: return "non-finite objective (lmshoot::NumericalError)";
+    case LMS_ERR_CUDA: return "CUDA failure";
+    case LMS_ERR_STATE: return "call order violated";
+    case LMS_ERR_COMM: return "NCCL failure";
+  }
+  return "unknown status";
+}
+
+const char* lms_variant_name(int precision, int variant)
+{
+  return lms::variant_name(precision, variant);
+}
+
+int lms_system_create(const lms_config* cfg, lms_system** out)
+{
+  if (!cfg || !out) return LMS_ERR_INVALID;
+  *out = nullptr;
+  if (cfg->dim != 2 && cfg->dim != 3) return LMS_ERR_SHAPE;  // shooting.hpp:358
+  if (!(cfg->sigma > 0)) return LMS_ERR_INVALID;             // shooting.hpp:113
+  if (cfg->precision != LMS_PRECISION_F32 && cfg->precision != LMS_PRECISION_F64) return LMS_ERR_INVALID;
+  if (cfg->max_timesteps < 1) return LMS_ERR_INVALID;
+  if (cfg->n > (size_t)0x7fffffff - 1024) return LMS_ERR_INVALID;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || cfg->device < 0 || cfg->device >= count) {
+    cudaGetLastError();
+    return LMS_ERR_CUDA;
+  }
+  lms_system* h = new (std::nothrow) lms_system;
+  if (!h) return LMS_ERR_CUDA;
+  h->device = cfg->device;
+  try {
+    h->impl = lms::create_system(*cfg);
+  } catch (const lms::StatusError& e) {
+    delete h;
+    return e.code;
+  } catch (...) {
+    cudaGetLastError();
+    delete h;
+    return LMS_ERR_CUDA;
+  }
+  *out = h;
+  return LMS_OK;
+}
+
+void lms_system_destroy(lms_system* sys)
+{
+  if (!sys) return;
+  delete sys->impl;
+  delete sys;
+}
+
+int lms_last_diverged_step(const lms_system* sys) { return sys && sys->impl ? sys->impl->last_diverged_step : -1; }
+long long lms_last_diverged_point(const lms_system* sys)
+{
+  return sys && sys->impl ? sys->impl->last_diverged_point : -1;
+}
+const char* lms_last_error_message(const lms_system* sys)
+{
+  return sys && sys->impl ? sys->impl->last_message.c_str() : "";
+}
+
+int lms_hamiltonian(lms_system* sys, const double* q, const double* p, double* out)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->hamiltonian(q, p, out); });
+}
+
+int lms_derivatives(lms_system* sys, const double* q, const double* p, double* hq, double* hp)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->derivatives(q, p, hq, hp); });
+}
+
+int lms_integrate_forward(lms_system* sys, const double* q0, const double* p0, int timesteps, double* traj_q,
+                          double* traj_p)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->integrate_forward(q0, p0, timesteps, traj_q, traj_p); });
+}
+
+int lms_adjoint_step(lms_system* sys, const double* q, const double* p, const double* alpha, const double* beta,
+                     double* d_alpha, double* d_beta)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->adjoint_step(q, p, alpha, beta, d_alpha, d_beta); });
+}
+
+int lms_mismatch_sq(lms_system* sys, const double* a, const double* b, double* out)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->mismatch_sq(a, b, out); });
+}
+
+int lms_bind_registration(lms_system* sys, const double* q0, const double* target, double lambda, int timesteps)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->bind(q0, target, lambda, timesteps); });
+}
+
+int lms_objective_eval(lms_system* sys, const double* x, double* grad, double* loss, double* kinetic,
+                       double* mismatch)
+{
+  double sc[3] = {0, 0, 0};
+  int rc = guarded(sys, [&](lms::SystemBase* s) { s->eval(x, grad, sc, false); });
+  if (rc == LMS_OK) {
+    if (loss) *loss = sc[0];
+    if (kinetic) *kinetic = sc[1];
+    if (mismatch) *mismatch = sc[2];
+  }
+  return rc;
+}
+
+int lms_objective_eval_device(lms_system* sys, const double* d_x, double* d_grad, double* scalars)
+{
+  double sc[3] = {0, 0, 0};
+  int rc = guarded(sys, [&](lms::SystemBase* s) { s->eval(d_x, d_grad, sc, true); });
+  if (rc == LMS_OK && scalars) std::memcpy(scalars, sc, sizeof(sc));
+  return rc;
+}
+
+int lms_compute_gradient(lms_system* sys, const double* q0, const double* p0, const double* target, double lambda,
+                         int timesteps, double* scalars, double* grad)
+{
+  return guarded(sys, [&](lms::SystemBase* s) {
+    s->bind(q0, target, lambda, timesteps);
+    double sc[3] = {0, 0, 0};
+    s->eval(p0, grad, sc, false);
+    if (scalars) std::memcpy(scalars, sc, sizeof(sc));
+  });
+}
+
+int lms_objective_final_q(lms_system* sys, double* out)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->final_q(out); });
+}
+
+double lms_last_eval_device_ms(const lms_system* sys) { return sys && sys->impl ? sys->impl->last_eval_ms : 0.0; }
+int lms_last_eval_kernel_launches(const lms_system* sys)
+{
+  return sys && sys->impl ? sys->impl->last_eval_launches : 0;
+}
+int lms_set_kernel_timing(lms_system* sys, int enabled)
+{
+  if (!sys || !sys->impl) return LMS_ERR_STATE;
+  sys->impl->kernel_timing = enabled != 0;
+  return LMS_OK;
+}
+double lms_last_kernel_ms(const lms_system* sys, int which)
+{
+  if (!sys || !sys->impl || which < 0 || which > 1) return 0.0;
+  return sys->impl->last_kernel_ms[which];
+}
+
+int lms_velocities(lms_system* sys, const double* q, const double* p, size_t m, const double* points, double* out)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->velocities(q, p, m, points, out); });
+}
+
+int lms_warp_points_stored(lms_system* sys, size_t m, const double* points, double* out)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->warp_stored(m, points, out); });
+}
+
+int lms_comm_unique_id(unsigned char id[128])
+{
+  const lms::NcclApi& nc = lms::nccl_api();
+  if (!nc.ok) return LMS_ERR_COMM;
+  lms::ncclUniqueId uid;
+  if (nc.GetUniqueId(&uid) != 0) return LMS_ERR_COMM;
+  std::memcpy(id, uid.internal, 128);
+  return LMS_OK;
+}
+
+int lms_system_comm_init(lms_system* sys, const unsigned char id[128], int rank, int world)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->comm_init(id, rank, world); });
+}
+
+// ---- register_impl core (registration.cpp:43-93) over the bound objective and lms_minimize ----
+static double bound_objective(void* user, const double* x, double* grad, size_t)
+{
+  lms_system* sys = static_cast<lms_system*>(user);
+  double loss = 0;
+  int rc = lms_objective_eval(sys, x, grad, &loss, nullptr, nullptr);
+  if (rc != LMS_OK) throw rc;  // unwinds through lms_minimize like DivergedError does through minimize
+  return loss;
+}
+
+int lms_register(lms_system* sys, const lms_lbfgs_params* params, double* momenta_out, double* warped_out,
+                 lms_minimize_result* result, double* hist_loss)
+{
+  if (!sys || !sys->impl) return LMS_ERR_STATE;
+  lms::SystemBase* s = sys->impl;
+  if (!s->bound) return LMS_ERR_STATE;
+  const size_t nd = s->host_q0.size();
+  std::vector<double> x0(nd), g(nd);
+  for (size_t e = 0; e < nd; ++e) x0[e] = (s->host_target[e] - s->host_q0[e]) / s->timesteps;  // registration.cpp:47-52
+  int rc;
+  try {
+    rc = lms_minimize(bound_objective, sys, nd, x0.data(), params, momenta_out, g.data(), result, hist_loss,
+                      nullptr, nullptr, nullptr);
+  } catch (int code) {
+    return code;
+  }
+  if (rc != LMS_OK) return rc;
+  // final re-integration under p0* (registration.cpp:85-93): one more evaluation leaves q(1) resident
+  double loss = 0;
+  rc = lms_objective_eval(sys, momenta_out, g.data(), &loss, nullptr, nullptr);
+  if (rc != LMS_OK) return rc;
+  return lms_objective_final_q(sys, warped_out);
+}
+
+// ---- synthetic inputs ----
+namespace {
+// rng.hpp:14-48: mt19937_64 with the explicit uniform / Box-Muller transforms (pairs, spare kept).
+struct Rng {
+  explicit Rng(uint64_t seed) : engine(seed) {}
+  double uniform() { return static_cast<double>(engine() >> 11) * 0x1.0p-53; }
+  double normal()
+  {
+    if (have_spare) {
+      have_spare = false;
+      return spare;
+    }
+    double u1 = 0.0;
+    while (u1 <= 0.0) u1 = uniform();
+    const double u2 = uniform();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double theta = 2.0 * 3.141592653589793238462643383279502884 * u2;
+    spare = r * std::sin(theta);
+    have_spare = true;
+    return r * std::cos(theta);
+  }
+  std::mt19937_64 engine;
+  bool have_spare = false;
+  double spare = 0.0;
+};
+}  // namespace
+
+void lms_rng_normals(uint64_t seed, size_t count, double* out)
+{
+  Rng rng(seed);
+  for (size_t i = 0; i < count; ++i) out[i] = rng.normal();
+}
+
+void lms_rng_uniforms(uint64_t seed, size_t count, double* out)
+{
+  Rng rng(seed);
+  for (size_t i = 0; i < count; ++i) out[i] = rng.uniform();
+}
+
+void lms_synth_sphere(size_t n, double extent, double* out)
+{
+  // Fibonacci sphere of diameter `extent`: z_i = 1 - 2(i+1/2)/n, theta_i = pi(3 - sqrt 5) i
+  const double radius = 0.5 * extent;
+  const double golden = 3.141592653589793238462643383279502884 * (3.0 - std::sqrt(5.0));
+  for (size_t i = 0; i < n; ++i) {
+    const double z = 1.0 - 2.0 * (double(i) + 0.5) / double(n);
+    const double r = std::sqrt(std::max(0.0, 1.0 - z * z));
+    const double th = golden * double(i);
+    out[3 * i + 0] = radius * r * std::cos(th);
+    out[3 * i + 1] = radius * r * std::sin(th);
+    out[3 * i + 2] = radius * z;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,577 @@
+// Fused pairwise-interaction kernels for landmark geodesic shooting on sm_100a.
+//
+// One kernel template covers the three O(N^2) row reductions of the reference:
+//   kFwd  derivatives            shooting.hpp:147-176 (term :158-169)
+//   kAdj  adjoint_step           shooting.hpp:233-271 (term :249-264)
+//   kVel  velocities_at_step     flow.hpp:26-48
+// K_ij is never materialised: each thread owns R rows, keeps their 2D (or D) running sums in
+// registers and sweeps j-tiles of the landmark state staged in shared memory.  The Euler update
+// (shooting.hpp:205-211 / :302-306), the finite check, the loss scalars (:286-288), the adjoint seed
+// (:290-296) and the final gradient (:309-313) run as epilogues of the same kernels.
+//
+// Data layout in HBM: component planes.  A "state" is 2*D planes (q_0..q_{D-1}, p_0..p_{D-1}) of
+// `stride` elements each; an "adjoint state" is 2*D planes (alpha, beta).  Planes are zero-padded
+// past n: a padded column has p = alpha = 0 and finite q, beta, so it contributes exact zeros to
+// every sum (SURVEY.md §7 "Padding").
+//
+// Work decomposition: the (row tile) x (j tile) cell grid is laid out row-major and cut into
+// gridDim.x equal contiguous ranges (stream-K), so every CTA does the same number of cells +-1
+// whatever N is.  A CTA whose range ends inside a row tile writes its partial sums to a slot; the
+// last CTA to arrive for that row tile (threadfence + counter) adds the slots in ascending j order
+// and runs the epilogue.  The combine order depends only on (n, grid), never on timing, so results
+// are bitwise reproducible run to run (reduction.hpp:38-40 promises the same of the CPU backends).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lms {
+
+constexpr int kThreads = 128;  // threads per CTA
+constexpr int kTileJ = 128;    // columns staged per shared-memory tile
+
+enum Mode : int { kFwd = 0, kAdj = 1, kVel = 2 };
+
+// Epilogue selector / flags.
+enum : unsigned {
+  kEpiRaw = 0u,        // write the row sums themselves (hq,hp | d_alpha,d_beta | v)
+  kEpiEuler = 1u,      // apply the explicit-Euler (or Euler-adjoint) update and store the new state
+  kEpiFirstStep = 2u,  // fwd: also store hp(q0,p0) and the per-tile partial of H = 1/2 sum p.hp
+  kEpiLastStep = 4u,   // fwd: also per-tile mismatch partial and the adjoint seed (alpha_T, beta_T)
+  kEpiGradOut = 8u,    // adj: also grad = beta_0 + hp(q0,p0) as row-major double
+};
+
+template <typename T>
+struct PairArgs {
+  // columns j: landmark state (and adjoint state for kAdj)
+  const T* jstate;
+  const T* jadj;
+  long long jstride;
+  int n_cols;
+  int n_j_tiles;
+  // rows i: for kFwd/kAdj the same arrays as the columns; for kVel the D planes of query points
+  const T* istate;
+  const T* iadj;
+  long long istride;
+  int n_rows;       // rows are valid for row < n_rows
+  int row_tile0;    // first row tile owned by this launch (row partition across GPUs)
+  int n_row_tiles;  // row tiles owned by this launch
+  // outputs
+  T* out;           // raw: sums planes; euler: next state / next adjoint state / moved points
+  long long ostride;
+  T* adj_seed;      // kEpiLastStep: adjoint state planes receiving (alpha_T, beta_T = 0)
+  T* hp0;           // kEpiFirstStep: D planes written; kEpiGradOut: D planes read
+  const T* target;  // kEpiLastStep: D planes
+  double* grad_out; // kEpiGradOut: row-major double n x D
+  double* h_part;   // per-row-tile partials of sum_i p_i . hp_i
+  double* mm_part;  // per-row-tile partials of sum_i |q_i(1) - target_i|^2
+  unsigned long long* diverged;  // atomicMin of (step << 32 | point)
+  // stream-K bookkeeping
+  T* partials;
+  int* counters;
+  int max_seg;
+  // constants, rounded on the host exactly as the reference rounds them (shooting.hpp:63-68,114-115,
+  // 196,293): kexp = k_scale * log2(e) for float (ex2.approx), k_scale itself for double.
+  T kexp;
+  T inv_sig2;
+  T dt;
+  T two_lambda;
+  unsigned epi;
+  int step;  // time step whose state this launch produces (for the divergence record)
+};
+
+// ---------------------------------------------------------------------------------------------
+// scalar math per working precision
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+struct Math;
+
+template <>
+struct Math<float> {
+  static __device__ __forceinline__ float kernel(float r2, float kexp)
+  {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(r2 * kexp));
+    return y;
+  }
+  static __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ bool finite(float a) { return isfinite(a); }
+};
+
+template <>
+struct Math<double> {
+  static __device__ __forceinline__ double kernel(double r2, double kexp) { return exp(r2 * kexp); }
+  static __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ bool finite(double a) { return isfinite(a); }
+};
+
+template <int MODE, int D>
+struct Shape {
+  static constexpr int kColComps = MODE == kAdj ? 4 * D : 2 * D;              // staged per column
+  static constexpr int kRowComps = MODE == kAdj ? 4 * D : (MODE == kFwd ? 2 * D : D);
+  static constexpr int kAcc = MODE == kVel ? D : 2 * D;                        // sums per row
+};
+
+// One pair (i, j).  ri: row operands [q, p, (alpha, beta)] or [x]; cj: column operands.
+// Forward accumulates  acc[0..D) += (p_i.p_j) K dx,  acc[D..2D) += K p_j   (hq = -inv_sig2 * acc[0..D)).
+// Adjoint accumulates  acc[0..D) += K (dx (c t - pa) - c db),  acc[D..2D) += K a_j - K t p_j
+//   with t = inv_sig2 (dx.db);  d_alpha = inv_sig2 * acc[0..D),  d_beta = acc[D..2D).
+template <typename T, int D, int MODE>
+__device__ __forceinline__ void pair_term(const T* __restrict__ ri, const T* __restrict__ cj,
+                                          T* __restrict__ acc, T kexp, T inv_sig2)
+{
+  T dx[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) dx[c] = ri[c] - cj[c];
+  T r2 = dx[0] * dx[0];
+#pragma unroll
+  for (int c = 1; c < D; ++c) r2 = fma(dx[c], dx[c], r2);
+  const T k = Math<T>::kernel(r2, kexp);
+  if constexpr (MODE == kVel) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[c] = fma(k, cj[D + c], acc[c]);
+  } else if constexpr (MODE == kFwd) {
+    T cc = ri[D] * cj[D];
+#pragma unroll
+    for (int c = 1; c < D; ++c) cc = fma(ri[D + c], cj[D + c], cc);
+    const T s = cc * k;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      acc[c] = fma(s, dx[c], acc[c]);
+      acc[D + c] = fma(k, cj[D + c], acc[D + c]);
+    }
+  } else {
+    const T* pi = ri + D;
+    const T* ai = ri + 2 * D;
+    const T* bi = ri + 3 * D;
+    const T* pj = cj + D;
+    const T* aj = cj + 2 * D;
+    const T* bj = cj + 3 * D;
+    T cc = pi[0] * pj[0];
+    T pa = pi[0] * aj[0];
+#pragma unroll
+    for (int c = 1; c < D; ++c) {
+      cc = fma(pi[c], pj[c], cc);
+      pa = fma(pi[c], aj[c], pa);
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) pa = fma(pj[c], ai[c], pa);
+    T db[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) db[c] = bj[c] - bi[c];
+    T rb = dx[0] * db[0];
+#pragma unroll
+    for (int c = 1; c < D; ++c) rb = fma(dx[c], db[c], rb);
+    const T t = rb * inv_sig2;
+    const T u = fma(cc, t, -pa);
+    const T ka = k * u;
+    const T kc = k * cc;
+    const T kt = k * t;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      acc[c] = fma(ka, dx[c], acc[c]);
+      acc[c] = fma(-kc, db[c], acc[c]);
+      acc[D + c] = fma(k, aj[c], acc[D + c]);
+      acc[D + c] = fma(-kt, pj[c], acc[D + c]);
+    }
+  }
+}
+
+// Vector load of JU consecutive columns of one staged component.
+template <typename T, int JU>
+struct ColVec;
+template <>
+struct ColVec<float, 4> {
+  static __device__ __forceinline__ void load(const float* p, float* v)
+  {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  }
+};
+template <>
+struct ColVec<float, 2> {
+  static __device__ __forceinline__ void load(const float* p, float* v)
+  {
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    v[0] = t.x; v[1] = t.y;
+  }
+};
+template <>
+struct ColVec<double, 2> {
+  static __device__ __forceinline__ void load(const double* p, double* v)
+  {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    v[0] = t.x; v[1] = t.y;
+  }
+};
+template <>
+struct ColVec<double, 1> {
+  static __device__ __forceinline__ void load(const double* p, double* v) { v[0] = *p; }
+};
+template <>
+struct ColVec<float, 1> {
+  static __device__ __forceinline__ void load(const float* p, float* v) { v[0] = *p; }
+};
+
+// Fixed-order block sum of one double per thread (tree over shared memory; deterministic).
+__device__ __forceinline__ double block_sum(double v, double* scratch)
+{
+  const int tid = threadIdx.x;
+  scratch[tid] = v;
+  __syncthreads();
+#pragma unroll
+  for (int h = kThreads / 2; h >= 1; h >>= 1) {
+    if (tid < h) scratch[tid] += scratch[tid + h];
+    __syncthreads();
+  }
+  const double r = scratch[0];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------------------------
+template <typename T, int D, int MODE, int R, int JU, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> a)
+{
+  using S = Shape<MODE, D>;
+  constexpr int NC = S::kColComps;
+  constexpr int NR = S::kRowComps;
+  constexpr int NA = S::kAcc;
+  constexpr int BM = kThreads * R;
+
+  __shared__ __align__(16) T tile[2][NC][kTileJ];
+  __shared__ double red_scratch[kThreads];
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x;
+  const long long nJ = a.n_j_tiles;
+  const long long cells = (long long)a.n_row_tiles * nJ;
+  const long long G = gridDim.x;
+  long long c = cells * blockIdx.x / G;
+  const long long c_end = cells * (blockIdx.x + 1) / G;
+  const long long first_rt_local = c / nJ;  // first row tile (local index) this CTA touches
+
+  // Column plane c of a tile: kAdj stages state planes [0,2D) then adjoint planes [0,2D).
+  auto col_plane = [&](int comp) -> const T* {
+    if constexpr (MODE == kAdj) {
+      return comp < 2 * D ? a.jstate + (long long)comp * a.jstride
+                          : a.jadj + (long long)(comp - 2 * D) * a.jstride;
+    } else {
+      return a.jstate + (long long)comp * a.jstride;
+    }
+  };
+
+  while (c < c_end) {
+    const long long rt_local = c / nJ;
+    const int jt0 = (int)(c - rt_local * nJ);
+    const long long span = c_end - c;
+    const int jt1 = (int)((long long)jt0 + span < nJ ? (long long)jt0 + span : nJ);
+    const int rt = a.row_tile0 + (int)rt_local;
+
+    // ---- row operands --------------------------------------------------------------------
+    T ri[R][NR];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long long row = (long long)rt * BM + r * kThreads + tid;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) {
+        if constexpr (MODE == kAdj) {
+          ri[r][k] = k < 2 * D ? a.istate[(long long)k * a.istride + row]
+                               : a.iadj[(long long)(k - 2 * D) * a.istride + row];
+        } else {
+          ri[r][k] = a.istate[(long long)k * a.istride + row];
+        }
+      }
+    }
+    T acc[R][NA];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int k = 0; k < NA; ++k) acc[r][k] = T(0);
+
+    // ---- sweep the j tiles [jt0, jt1) with register-prefetched double buffering ---------------
+    T stage[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)jt0 * kTileJ + tid];
+    int buf = 0;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) tile[0][k][tid] = stage[k];
+    __syncthreads();
+    for (int jt = jt0; jt < jt1; ++jt) {
+      const bool more = jt + 1 < jt1;
+      if (more) {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)(jt + 1) * kTileJ + tid];
+      }
+#pragma unroll 1
+      for (int jj = 0; jj < kTileJ; jj += JU) {
+        T cj[JU][NC];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          T v[JU];
+          ColVec<T, JU>::load(&tile[buf][k][jj], v);
+#pragma unroll
+          for (int u = 0; u < JU; ++u) cj[u][k] = v[u];
+        }
+#pragma unroll
+        for (int u = 0; u < JU; ++u)
+#pragma unroll
+          for (int r = 0; r < R; ++r) pair_term<T, D, MODE>(ri[r], cj[u], acc[r], a.kexp, a.inv_sig2);
+      }
+      if (more) {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) tile[buf ^ 1][k][tid] = stage[k];
+      }
+      __syncthreads();
+      buf ^= 1;
+    }
+
+    // ---- combine partial sums across the CTAs that share this row tile ----------------------------
+    const long long cell_lo = rt_local * nJ;
+    const long long cell_hi = cell_lo + nJ - 1;
+    const long long cta_first = ((cell_lo + 1) * G - 1) / cells;
+    const long long cta_last = ((cell_hi + 1) * G - 1) / cells;
+    bool do_epilogue = true;
+    if (cta_first != cta_last) {
+      const long long slot = (long long)blockIdx.x * a.max_seg + (rt_local - first_rt_local);
+      T* mine = a.partials + slot * (NA * BM);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int k = 0; k < NA; ++k) __stcg(mine + k * BM + r * kThreads + tid, acc[r][k]);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const int nseg = (int)(cta_last - cta_first + 1);
+        const int prev = atomicAdd(a.counters + rt_local, 1);
+        const int last = prev == nseg - 1;
+        if (last) a.counters[rt_local] = 0;  // everyone has arrived: re-arm for the next launch
+        s_last = last;
+      }
+      __syncthreads();
+      do_epilogue = s_last != 0;
+      if (do_epilogue) {
+        __threadfence();
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int k = 0; k < NA; ++k) acc[r][k] = T(0);
+        for (long long cta = cta_first; cta <= cta_last; ++cta) {
+          const long long cb = cells * cta / G;
+          const long long s = cta * a.max_seg + (rt_local - cb / nJ);
+          const T* theirs = a.partials + s * (NA * BM);
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int k = 0; k < NA; ++k) acc[r][k] += __ldcg(theirs + k * BM + r * kThreads + tid);
+        }
+      }
+    }
+
+    // ---- epilogue ----------------------------------------------------------------------------
+    if (do_epilogue) {
+      double hsum = 0.0, msum = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long row = (long long)rt * BM + r * kThreads + tid;
+        const bool live = row < a.n_rows;
+        if constexpr (MODE == kVel) {
+          if (live) {
+            if (a.epi & kEpiEuler) {
+              bool ok = true;
+#pragma unroll
+              for (int k = 0; k < D; ++k) {
+                const T xn = Math<T>::add_rn(ri[r][k], Math<T>::mul_rn(a.dt, acc[r][k]));
+                ok = ok && Math<T>::finite(xn);
+                a.out[(long long)k * a.ostride + row] = xn;
+              }
+              if (!ok)
+                atomicMin(a.diverged, ((unsigned long long)(unsigned)a.step << 32) | (unsigned long long)row);
+            } else {
+#pragma unroll
+              for (int k = 0; k < D; ++k) a.out[(long long)k * a.ostride + row] = acc[r][k];
+            }
+          }
+        } else if constexpr (MODE == kFwd) {
+          T hq[D], hp[D];
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            hq[k] = -a.inv_sig2 * acc[r][k];
+            hp[k] = acc[r][D + k];
+          }
+          if (live) {
+            if (a.epi & kEpiEuler) {
+              bool ok = true;
+              T qn[D];
+#pragma unroll
+              for (int k = 0; k < D; ++k) {
+                // q_{t+1} = q_t + dt*hp ; p_{t+1} = p_t - dt*hq   (shooting.hpp:205-209)
+                qn[k] = Math<T>::add_rn(ri[r][k], Math<T>::mul_rn(a.dt, hp[k]));
+                const T pn = Math<T>::add_rn(ri[r][D + k], -Math<T>::mul_rn(a.dt, hq[k]));
+                ok = ok && Math<T>::finite(qn[k]) && Math<T>::finite(pn);
+                a.out[(long long)k * a.ostride + row] = qn[k];
+                a.out[(long long)(D + k) * a.ostride + row] = pn;
+              }
+              if (!ok) atomicMin(a.diverged, ((unsigned long long)(unsigned)a.step << 32) | 0xffffffffull);
+              if (a.epi & kEpiFirstStep) {
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                  a.hp0[(long long)k * a.ostride + row] = hp[k];
+                  hsum += (double)ri[r][D + k] * (double)hp[k];
+                }
+              }
+              if (a.epi & kEpiLastStep) {
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                  const T tg = a.target[(long long)k * a.ostride + row];
+                  const double df = (double)qn[k] - (double)tg;  // shooting.hpp:324-325
+                  msum += df * df;
+                  // alpha_T = 2*lambda*(q(1) - target), beta_T = 0   (shooting.hpp:290-296)
+                  a.adj_seed[(long long)k * a.ostride + row] = Math<T>::mul_rn(a.two_lambda, qn[k] - tg);
+                  a.adj_seed[(long long)(D + k) * a.ostride + row] = T(0);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < D; ++k) {
+                a.out[(long long)k * a.ostride + row] = hq[k];
+                a.out[(long long)(D + k) * a.ostride + row] = hp[k];
+                if (a.epi & kEpiFirstStep) hsum += (double)ri[r][D + k] * (double)hp[k];
+              }
+            }
+          }
+        } else {
+          if (live) {
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              const T da = a.inv_sig2 * acc[r][k];
+              const T dbeta = acc[r][D + k];
+              if (a.epi & kEpiEuler) {
+                // alpha += dt*d_alpha ; beta += dt*d_beta   (shooting.hpp:302-306)
+                const T an = Math<T>::add_rn(ri[r][2 * D + k], Math<T>::mul_rn(a.dt, da));
+                const T bn = Math<T>::add_rn(ri[r][3 * D + k], Math<T>::mul_rn(a.dt, dbeta));
+                a.out[(long long)k * a.ostride + row] = an;
+                a.out[(long long)(D + k) * a.ostride + row] = bn;
+                if (a.epi & kEpiGradOut)  // grad = beta_0 + hp(q0,p0)   (shooting.hpp:311-313)
+                  a.grad_out[row * D + k] =
+                      (double)Math<T>::add_rn(bn, a.hp0[(long long)k * a.ostride + row]);
+              } else {
+                a.out[(long long)k * a.ostride + row] = da;
+                a.out[(long long)(D + k) * a.ostride + row] = dbeta;
+              }
+            }
+          }
+        }
+      }
+      if constexpr (MODE == kFwd) {
+        // block-uniform flags: every thread takes the same branch around the barriers in block_sum
+        if (a.epi & kEpiFirstStep) {
+          const double h = block_sum(hsum, red_scratch);
+          if (tid == 0) a.h_part[(long long)rt * R] = h;  // indexed in 128-row units
+        }
+        if (a.epi & kEpiLastStep) {
+          const double m = block_sum(msum, red_scratch);
+          if (tid == 0) a.mm_part[(long long)rt * R] = m;
+        }
+      }
+    }
+    c += jt1 - jt0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// O(N) helpers
+// ---------------------------------------------------------------------------------------------
+
+// Row-major double (n x ncomp) -> ncomp planes of T, cast T(x) as registration.cpp:63 does.
+// Non-finite inputs record divergence at `step` (integrate_forward's entry check, shooting.hpp:185-186).
+template <typename T>
+__global__ void aos_to_planes(const double* __restrict__ src, T* __restrict__ dst, long long stride,
+                              int n, int ncomp, unsigned long long* diverged, int step)
+{
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * ncomp) return;
+  const int i = (int)(e / ncomp);
+  const int c = (int)(e - (long long)i * ncomp);
+  const T v = (T)src[e];
+  dst[(long long)c * stride + i] = v;
+  if (diverged != nullptr && !isfinite(v))
+    atomicMin(diverged, ((unsigned long long)(unsigned)step << 32) | 0xffffffffull);
+}
+
+template <typename T>
+__global__ void planes_to_aos(const T* __restrict__ src, long long stride, double* __restrict__ dst, int n,
+                              int ncomp)
+{
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * ncomp) return;
+  const int i = (int)(e / ncomp);
+  const int c = (int)(e - (long long)i * ncomp);
+  dst[e] = (double)src[(long long)c * stride + i];
+}
+
+// Plane-to-plane copy of the live rows (device-resident snapshot 0 <- bound q0).
+template <typename T>
+__global__ void copy_planes(const T* __restrict__ src, long long sstride, T* __restrict__ dst, long long dstride,
+                            int n, int ncomp)
+{
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * ncomp) return;
+  const int c = (int)(e / n);
+  const int i = (int)(e - (long long)c * n);
+  dst[(long long)c * dstride + i] = src[(long long)c * sstride + i];
+}
+
+// Finite check of state planes (q0/p0 entry check, shooting.hpp:185-186).
+template <typename T>
+__global__ void check_finite_planes(const T* __restrict__ src, long long stride, int n, int ncomp,
+                                    unsigned long long* diverged, int step)
+{
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * ncomp) return;
+  const int c = (int)(e / n);
+  const int i = (int)(e - (long long)c * n);
+  if (!isfinite(src[(long long)c * stride + i]))
+    atomicMin(diverged, ((unsigned long long)(unsigned)step << 32) | 0xffffffffull);
+}
+
+// scalars[0..2] = {loss, kinetic, mismatch}: fixed ascending sum of the per-row-tile partials
+// (loss = H + lambda*mismatch, shooting.hpp:286-288; H = 1/2 sum_i p_i . hp_i).
+template <int kUnused = 0>
+__global__ void finalize_scalars(const double* __restrict__ h_part, const double* __restrict__ mm_part,
+                                 int n_tiles, double lambda, double* __restrict__ scalars)
+{
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double h = 0.0, m = 0.0;
+  for (int t = 0; t < n_tiles; ++t) {
+    h += h_part[t];
+    m += mm_part[t];
+  }
+  h *= 0.5;
+  scalars[1] = h;
+  scalars[2] = m;
+  scalars[0] = h + lambda * m;
+}
+
+// Strictly sequential double sum of squared differences over row-major-equivalent order
+// (mismatch_sq, shooting.hpp:318-329): one thread, element order i-major then c, as the reference.
+template <typename T>
+__global__ void mismatch_sequential(const T* __restrict__ a, const T* __restrict__ b, long long stride, int n,
+                                    int ncomp, double* __restrict__ out)
+{
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < ncomp; ++c) {
+      // explicit _rn ops: no FMA contraction, so the sum is bit-identical to the reference's loop
+      const double d = __dadd_rn((double)a[(long long)c * stride + i], -(double)b[(long long)c * stride + i]);
+      s = __dadd_rn(s, __dmul_rn(d, d));
+    }
+  *out = s;
+}
+
+}  // namespace lms

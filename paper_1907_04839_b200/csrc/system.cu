@@ -1,0 +1,825 @@
+// System<T,D>: implementation.  See system.cuh.
+#include "system.cuh"
+
+namespace lms {
+
+namespace {
+
+inline long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+template <typename T>
+T* dev_alloc_zero(size_t count)
+{
+  T* p = nullptr;
+  LMS_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  LMS_CUDA(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)));
+  return p;
+}
+
+template <typename T>
+void dev_free(T*& p)
+{
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+}  // namespace
+
+// ---- kernel variant tables -------------------------------------------------------------------------
+// (R rows per thread, JU columns per shared-memory vector load, min CTAs/SM for __launch_bounds__).
+// Variant 0 is the default the library ships with; the rest are kept for on-GPU A/B (bench.py --variant).
+#define LMS_PICK(T, D, MODE, R, JU, MINB, NAME) make_choice<T, D, MODE, R, JU, MINB>(NAME)
+
+template <>
+KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
+{
+  switch (v) {
+    case 1: return LMS_PICK(float, 3, kFwd, 2, 4, 4, "fwd_f32_r2_j4");
+    case 2: return LMS_PICK(float, 3, kFwd, 4, 2, 3, "fwd_f32_r4_j2");
+    case 3: return LMS_PICK(float, 3, kFwd, 2, 2, 6, "fwd_f32_r2_j2");
+    default: return LMS_PICK(float, 3, kFwd, 4, 4, 3, "fwd_f32_r4_j4");
+  }
+}
+template <>
+KernelChoice<float> pick_kernel<float, 3, kAdj>(int v)
+{
+  switch (v) {
+    case 1: return LMS_PICK(float, 3, kAdj, 2, 4, 3, "adj_f32_r2_j4");
+    case 2: return LMS_PICK(float, 3, kAdj, 4, 2, 2, "adj_f32_r4_j2");
+    case 3: return LMS_PICK(float, 3, kAdj, 1, 4, 6, "adj_f32_r1_j4");
+    default: return LMS_PICK(float, 3, kAdj, 2, 2, 4, "adj_f32_r2_j2");
+  }
+}
+template <>
+KernelChoice<float> pick_kernel<float, 3, kVel>(int)
+{
+  return LMS_PICK(float, 3, kVel, 4, 4, 4, "vel_f32_r4_j4");
+}
+template <>
+KernelChoice<double> pick_kernel<double, 3, kFwd>(int v)
+{
+  switch (v) {
+    case 1: return LMS_PICK(double, 3, kFwd, 1, 2, 4, "fwd_f64_r1_j2");
+    case 2: return LMS_PICK(double, 3, kFwd, 4, 2, 2, "fwd_f64_r4_j2");
+    default: return LMS_PICK(double, 3, kFwd, 2, 2, 3, "fwd_f64_r2_j2");
+  }
+}
+template <>
+KernelChoice<double> pick_kernel<double, 3, kAdj>(int v)
+{
+  switch (v) {
+    case 1: return LMS_PICK(double, 3, kAdj, 1, 2, 3, "adj_f64_r1_j2");
+    case 2: return LMS_PICK(double, 3, kAdj, 2, 1, 2, "adj_f64_r2_j1");
+    default: return LMS_PICK(double, 3, kAdj, 2, 2, 2, "adj_f64_r2_j2");
+  }
+}
+template <>
+KernelChoice<double> pick_kernel<double, 3, kVel>(int)
+{
+  return LMS_PICK(double, 3, kVel, 2, 2, 4, "vel_f64_r2_j2");
+}
+template <>
+KernelChoice<float> pick_kernel<float, 2, kFwd>(int)
+{
+  return LMS_PICK(float, 2, kFwd, 4, 4, 3, "fwd_f32_d2_r4_j4");
+}
+template <>
+KernelChoice<float> pick_kernel<float, 2, kAdj>(int)
+{
+  return LMS_PICK(float, 2, kAdj, 2, 2, 4, "adj_f32_d2_r2_j2");
+}
+template <>
+KernelChoice<float> pick_kernel<float, 2, kVel>(int)
+{
+  return LMS_PICK(float, 2, kVel, 4, 4, 4, "vel_f32_d2_r4_j4");
+}
+template <>
+KernelChoice<double> pick_kernel<double, 2, kFwd>(int)
+{
+  return LMS_PICK(double, 2, kFwd, 2, 2, 3, "fwd_f64_d2_r2_j2");
+}
+template <>
+KernelChoice<double> pick_kernel<double, 2, kAdj>(int)
+{
+  return LMS_PICK(double, 2, kAdj, 2, 2, 2, "adj_f64_d2_r2_j2");
+}
+template <>
+KernelChoice<double> pick_kernel<double, 2, kVel>(int)
+{
+  return LMS_PICK(double, 2, kVel, 2, 2, 4, "vel_f64_d2_r2_j2");
+}
+
+// ---- construction ------------------------------------------------------------------------------------
+template <typename T, int D>
+System<T, D>::System(const lms_config& c)
+{
+  cfg = c;
+  LMS_CUDA(cudaSetDevice(c.device));
+  cudaDeviceProp prop;
+  LMS_CUDA(cudaGetDeviceProperties(&prop, c.device));
+  if (prop.major != 10) throw StatusError{LMS_ERR_CUDA, "device is not sm_100 (B200); no fallback path exists"};
+  num_sms_ = prop.multiProcessorCount;
+  LMS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  LMS_CUDA(cudaEventCreate(&ev_begin_));
+  LMS_CUDA(cudaEventCreate(&ev_end_));
+
+  // Constants rounded as the reference rounds them (shooting.hpp:63-68,114-115).
+  inv_sig2_ = T(1) / (T(c.sigma) * T(c.sigma));
+  const T k_scale = T(-0.5) * inv_sig2_;
+  if constexpr (sizeof(T) == 4)
+    kexp_ = (T)((double)k_scale * 1.4426950408889634074);  // ex2.approx: exp(x) = 2^(x log2 e)
+  else
+    kexp_ = k_scale;
+
+  k_fwd_ = pick_kernel<T, D, kFwd>(c.variant);
+  k_adj_ = pick_kernel<T, D, kAdj>(c.variant);
+  k_vel_ = pick_kernel<T, D, kVel>(c.variant);
+
+  max_t_ = std::max(c.max_timesteps, 1);
+  const long long N = (long long)c.n;
+  stride_ = std::max<long long>(round_up(N, kRowAlign), kRowAlign);
+  const size_t plane = (size_t)stride_;
+  traj_ = dev_alloc_zero<T>((size_t)(max_t_ + 1) * kState * plane);
+  adj_[0] = dev_alloc_zero<T>(kState * plane);
+  adj_[1] = dev_alloc_zero<T>(kState * plane);
+  hp0_ = dev_alloc_zero<T>(D * plane);
+  target_ = dev_alloc_zero<T>(D * plane);
+  q0_ = dev_alloc_zero<T>(D * plane);
+  scratch_in_ = dev_alloc_zero<T>(2 * kState * plane);
+  scratch_out_ = dev_alloc_zero<T>(kState * plane);
+  d_scalars_ = dev_alloc_zero<double>(4);
+  d_diverged_ = reinterpret_cast<unsigned long long*>(d_scalars_ + 3);
+  io_cap_ = (size_t)N * D;
+  d_io_ = dev_alloc_zero<double>(4 * io_cap_);
+  d_x_ = dev_alloc_zero<double>((size_t)stride_ * D);
+  d_grad_ = dev_alloc_zero<double>((size_t)stride_ * D);
+  LMS_CUDA(cudaMallocHost(&h_scalars_, 4 * sizeof(double)));
+  part_tiles_ = (int)(stride_ / kThreads);
+  h_part_ = dev_alloc_zero<double>(part_tiles_);
+  mm_part_ = dev_alloc_zero<double>(part_tiles_);
+}
+
+template <typename T, int D>
+System<T, D>::~System()
+{
+  cudaSetDevice(cfg.device);
+  if (stream_) cudaStreamSynchronize(stream_);
+  destroy_graph();
+  if (comm_ && nccl_api().ok) nccl_api().CommDestroy(comm_);
+  dev_free(traj_);
+  dev_free(adj_[0]);
+  dev_free(adj_[1]);
+  dev_free(hp0_);
+  dev_free(target_);
+  dev_free(q0_);
+  dev_free(scratch_in_);
+  dev_free(scratch_out_);
+  dev_free(points_[0]);
+  dev_free(points_[1]);
+  dev_free(partials_);
+  dev_free(counters_);
+  dev_free(h_part_);
+  dev_free(mm_part_);
+  dev_free(d_scalars_);
+  dev_free(d_io_);
+  dev_free(d_x_);
+  dev_free(d_grad_);
+  if (h_scalars_) cudaFreeHost(h_scalars_);
+  for (auto e : events_) cudaEventDestroy(e);
+  if (ev_begin_) cudaEventDestroy(ev_begin_);
+  if (ev_end_) cudaEventDestroy(ev_end_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+template <typename T, int D>
+void System<T, D>::destroy_graph()
+{
+  if (graph_) cudaGraphExecDestroy(graph_);
+  graph_ = nullptr;
+}
+
+// ---- launch planning -----------------------------------------------------------------------------------
+template <typename T, int D>
+int System<T, D>::row_tile_begin_(int bm) const
+{
+  const long long slice = stride_ / world_;  // rows per rank, a multiple of kRowAlign
+  return (int)(rank_ * slice / bm);
+}
+
+template <typename T, int D>
+int System<T, D>::row_tile_end_(int bm) const
+{
+  const long long slice = stride_ / world_;
+  const int live_tiles = ceil_div((long long)cfg.n, bm);
+  return std::min<int>((int)((rank_ + 1) * slice / bm), live_tiles);
+}
+
+template <typename T, int D>
+template <int MODE>
+LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_tile0, int row_tiles)
+{
+  LaunchPlan p;
+  p.bm = kThreads * k.rows_per_thread;
+  p.n_row_tiles = row_tiles >= 0 ? row_tiles : ceil_div(n_rows, p.bm);
+  p.n_j_tiles = ceil_div((long long)cfg.n, kTileJ);
+  (void)row_tile0;
+  const long long cells = (long long)p.n_row_tiles * p.n_j_tiles;
+  if (cells <= 0) return p;
+  int per_sm = 0;
+  LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kThreads, 0));
+  per_sm = std::max(per_sm, 1);
+  const long long full = (long long)num_sms_ * per_sm;
+  p.grid = (int)std::min<long long>(full, cells);
+  const long long per_cta = (cells + p.grid - 1) / p.grid;
+  p.max_seg = (int)((per_cta + p.n_j_tiles - 1) / p.n_j_tiles) + 1;
+  constexpr int NA = Shape<MODE, D>::kAcc;
+  p.partial_elems = (size_t)p.grid * p.max_seg * NA * p.bm;
+  return p;
+}
+
+template <typename T, int D>
+void System<T, D>::ensure_partials(size_t elems, int row_tiles)
+{
+  if (elems > partials_cap_) {
+    sync();
+    dev_free(partials_);
+    partials_ = dev_alloc_zero<T>(elems);
+    partials_cap_ = elems;
+  }
+  if (row_tiles > counters_cap_) {
+    sync();
+    dev_free(counters_);
+    counters_ = dev_alloc_zero<int>(row_tiles);
+    counters_cap_ = row_tiles;
+  }
+}
+
+template <typename T, int D>
+PairArgs<T> System<T, D>::base_args() const
+{
+  PairArgs<T> a{};
+  a.jstride = stride_;
+  a.istride = stride_;
+  a.ostride = stride_;
+  a.n_cols = n();
+  a.n_rows = n();
+  a.row_tile0 = 0;
+  a.hp0 = hp0_;
+  a.target = target_;
+  a.grad_out = d_grad_;
+  a.h_part = h_part_;
+  a.mm_part = mm_part_;
+  a.diverged = d_diverged_;
+  a.kexp = kexp_;
+  a.inv_sig2 = inv_sig2_;
+  a.dt = dt_;
+  a.two_lambda = two_lambda_;
+  a.epi = kEpiRaw;
+  a.step = 0;
+  return a;
+}
+
+template <typename T, int D>
+template <int MODE>
+void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchPlan& plan)
+{
+  if (plan.grid <= 0) return;
+  a.n_row_tiles = plan.n_row_tiles;
+  a.n_j_tiles = plan.n_j_tiles;
+  a.max_seg = plan.max_seg;
+  a.partials = partials_;
+  a.counters = counters_;
+  k.fn<<<plan.grid, kThreads, 0, stream_>>>(a);
+  LMS_CUDA(cudaGetLastError());
+  ++last_eval_launches;
+}
+
+// ---- host <-> planes ---------------------------------------------------------------------------------------
+template <typename T, int D>
+void System<T, D>::upload(const double* host, T* planes, long long stride, int count, int ncomp, bool check,
+                          int step)
+{
+  if (count <= 0) return;
+  const size_t elems = (size_t)count * ncomp;
+  if (elems > io_cap_) {
+    sync();
+    dev_free(d_io_);
+    io_cap_ = elems;
+    d_io_ = dev_alloc_zero<double>(4 * io_cap_);
+  }
+  LMS_CUDA(cudaMemcpyAsync(d_io_, host, elems * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  const int blocks = ceil_div((long long)elems, 256);
+  aos_to_planes<T><<<blocks, 256, 0, stream_>>>(d_io_, planes, stride, count, ncomp, check ? d_diverged_ : nullptr,
+                                                step);
+  LMS_CUDA(cudaGetLastError());
+}
+
+template <typename T, int D>
+void System<T, D>::download(const T* planes, long long stride, double* host, int count, int ncomp)
+{
+  if (count <= 0) return;
+  const size_t elems = (size_t)count * ncomp;
+  if (elems > io_cap_) {
+    sync();
+    dev_free(d_io_);
+    io_cap_ = elems;
+    d_io_ = dev_alloc_zero<double>(4 * io_cap_);
+  }
+  const int blocks = ceil_div((long long)elems, 256);
+  planes_to_aos<T><<<blocks, 256, 0, stream_>>>(planes, stride, d_io_ + io_cap_, count, ncomp);
+  LMS_CUDA(cudaGetLastError());
+  LMS_CUDA(cudaMemcpyAsync(host, d_io_ + io_cap_, elems * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+}
+
+template <typename T, int D>
+void System<T, D>::reset_diverged()
+{
+  LMS_CUDA(cudaMemsetAsync(d_diverged_, 0xff, sizeof(unsigned long long), stream_));
+}
+
+template <typename T, int D>
+void System<T, D>::read_diverged_or_throw()
+{
+  LMS_CUDA(cudaMemcpyAsync(h_scalars_, d_scalars_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  unsigned long long word;
+  std::memcpy(&word, h_scalars_ + 3, sizeof(word));
+  if (word != kNotDiverged) {
+    last_diverged_step = (int)(word >> 32);
+    const unsigned low = (unsigned)(word & 0xffffffffull);
+    last_diverged_point = low == 0xffffffffu ? -1 : (long long)low;
+    throw StatusError{LMS_ERR_DIVERGED, "non-finite state during integration"};
+  }
+}
+
+// ---- HamiltonianSystem members ----------------------------------------------------------------------------------
+template <typename T, int D>
+void System<T, D>::derivatives(const double* q, const double* p, double* hq, double* hp)
+{
+  if (n() == 0) return;
+  upload(q, scratch_in_, stride_, n(), D, false, 0);
+  upload(p, scratch_in_ + D * stride_, stride_, n(), D, false, 0);
+  LaunchPlan plan = plan_for<kFwd>(k_fwd_, n());
+  ensure_partials(plan.partial_elems, plan.n_row_tiles);
+  PairArgs<T> a = base_args();
+  a.jstate = a.istate = scratch_in_;
+  a.out = scratch_out_;
+  launch<kFwd>(k_fwd_, a, plan);
+  download(scratch_out_, stride_, hq, n(), D);
+  sync();
+  download(scratch_out_ + D * stride_, stride_, hp, n(), D);
+  sync();
+}
+
+template <typename T, int D>
+void System<T, D>::hamiltonian(const double* q, const double* p, double* out)
+{
+  *out = 0.0;
+  if (n() == 0) return;
+  upload(q, scratch_in_, stride_, n(), D, false, 0);
+  upload(p, scratch_in_ + D * stride_, stride_, n(), D, false, 0);
+  LaunchPlan plan = plan_for<kFwd>(k_fwd_, n());
+  ensure_partials(plan.partial_elems, plan.n_row_tiles);
+  PairArgs<T> a = base_args();
+  a.jstate = a.istate = scratch_in_;
+  a.out = scratch_out_;
+  a.epi = kEpiRaw | kEpiFirstStep;
+  launch<kFwd>(k_fwd_, a, plan);
+  finalize_scalars<0><<<1, 32, 0, stream_>>>(h_part_, mm_part_, plan.n_row_tiles, 0.0, d_scalars_);
+  LMS_CUDA(cudaGetLastError());
+  LMS_CUDA(cudaMemcpyAsync(h_scalars_, d_scalars_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  *out = h_scalars_[1];
+}
+
+template <typename T, int D>
+void System<T, D>::adjoint_step(const double* q, const double* p, const double* alpha, const double* beta,
+                                double* da, double* db)
+{
+  if (n() == 0) return;
+  upload(q, scratch_in_, stride_, n(), D, false, 0);
+  upload(p, scratch_in_ + D * stride_, stride_, n(), D, false, 0);
+  upload(alpha, scratch_in_ + 2 * D * stride_, stride_, n(), D, false, 0);
+  upload(beta, scratch_in_ + 3 * D * stride_, stride_, n(), D, false, 0);
+  LaunchPlan plan = plan_for<kAdj>(k_adj_, n());
+  ensure_partials(plan.partial_elems, plan.n_row_tiles);
+  PairArgs<T> a = base_args();
+  a.jstate = a.istate = scratch_in_;
+  a.jadj = a.iadj = scratch_in_ + kState * stride_;
+  a.out = scratch_out_;
+  launch<kAdj>(k_adj_, a, plan);
+  download(scratch_out_, stride_, da, n(), D);
+  sync();
+  download(scratch_out_ + D * stride_, stride_, db, n(), D);
+  sync();
+}
+
+template <typename T, int D>
+void System<T, D>::mismatch_sq(const double* a, const double* b, double* out)
+{
+  *out = 0.0;
+  if (n() == 0) return;
+  upload(a, scratch_in_, stride_, n(), D, false, 0);
+  upload(b, scratch_in_ + D * stride_, stride_, n(), D, false, 0);
+  mismatch_sequential<T><<<1, 32, 0, stream_>>>(scratch_in_, scratch_in_ + D * stride_, stride_, n(), D,
+                                                d_scalars_ + 2);
+  LMS_CUDA(cudaGetLastError());
+  LMS_CUDA(cudaMemcpyAsync(h_scalars_, d_scalars_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  *out = h_scalars_[2];
+}
+
+template <typename T, int D>
+void System<T, D>::integrate_forward(const double* q0, const double* p0, int timesteps, double* tq, double* tp)
+{
+  if (timesteps < 1) throw StatusError{LMS_ERR_INVALID, "timesteps must be >= 1"};
+  if (timesteps > max_t_) throw StatusError{LMS_ERR_INVALID, "timesteps exceeds cfg.max_timesteps"};
+  if (world_ > 1) throw StatusError{LMS_ERR_STATE, "integrate_forward is single-GPU; use the bound objective"};
+  stored_t_ = -1;
+  traj0_is_q0_ = false;
+  if (n() == 0) {
+    stored_t_ = timesteps;
+    return;
+  }
+  reset_diverged();
+  upload(q0, snapshot(0), stride_, n(), D, true, 0);
+  upload(p0, snapshot(0) + D * stride_, stride_, n(), D, true, 0);
+  LaunchPlan plan = plan_for<kFwd>(k_fwd_, n());
+  ensure_partials(plan.partial_elems, plan.n_row_tiles);
+  const T dt = T(1.0 / timesteps);  // shooting.hpp:190,196
+  for (int t = 0; t < timesteps; ++t) {
+    PairArgs<T> a = base_args();
+    a.jstate = a.istate = snapshot(t);
+    a.out = snapshot(t + 1);
+    a.dt = dt;
+    a.epi = kEpiEuler;
+    a.step = t + 1;
+    launch<kFwd>(k_fwd_, a, plan);
+  }
+  read_diverged_or_throw();
+  stored_t_ = timesteps;
+  for (int t = 0; t <= timesteps; ++t) {
+    if (tq) {
+      download(snapshot(t), stride_, tq + (size_t)t * n() * D, n(), D);
+      sync();
+    }
+    if (tp) {
+      download(snapshot(t) + D * stride_, stride_, tp + (size_t)t * n() * D, n(), D);
+      sync();
+    }
+  }
+}
+
+// ---- the bound objective ----------------------------------------------------------------------------------------
+template <typename T, int D>
+void System<T, D>::bind(const double* q0, const double* target, double lambda_in, int timesteps_in)
+{
+  if (timesteps_in < 1) throw StatusError{LMS_ERR_INVALID, "timesteps must be >= 1"};
+  if (timesteps_in > max_t_) throw StatusError{LMS_ERR_INVALID, "timesteps exceeds cfg.max_timesteps"};
+  if (!(lambda_in >= 0)) throw StatusError{LMS_ERR_INVALID, "lambda must be >= 0"};
+  sync();
+  destroy_graph();
+  bound = false;
+  lambda = lambda_in;
+  timesteps = timesteps_in;
+  host_q0.assign(q0, q0 + (size_t)n() * D);
+  host_target.assign(target, target + (size_t)n() * D);
+  dt_ = T(1.0 / timesteps);              // shooting.hpp:190,196,298
+  two_lambda_ = T(2) * T(lambda);        // shooting.hpp:293
+  q0_bad_ = false;
+  for (double v : host_q0)
+    if (!std::isfinite((double)(T)v)) q0_bad_ = true;
+  traj0_is_q0_ = false;
+  stored_t_ = -1;
+  if (n() > 0) {
+    upload(q0, q0_, stride_, n(), D, false, 0);
+    upload(target, target_, stride_, n(), D, false, 0);
+    const int tb_f = row_tile_begin_(kThreads * k_fwd_.rows_per_thread);
+    const int te_f = row_tile_end_(kThreads * k_fwd_.rows_per_thread);
+    const int tb_a = row_tile_begin_(kThreads * k_adj_.rows_per_thread);
+    const int te_a = row_tile_end_(kThreads * k_adj_.rows_per_thread);
+    plan_fwd_ = plan_for<kFwd>(k_fwd_, n(), tb_f, std::max(te_f - tb_f, 0));
+    plan_adj_ = plan_for<kAdj>(k_adj_, n(), tb_a, std::max(te_a - tb_a, 0));
+    ensure_partials(std::max(plan_fwd_.partial_elems, plan_adj_.partial_elems),
+                    std::max(plan_fwd_.n_row_tiles, plan_adj_.n_row_tiles));
+    sync();
+    if (world_ == 1) {
+      // Capture the whole evaluation (2T+2 kernels) into one CUDA graph: at small N the 2T dependent
+      // launches are pure latency (SURVEY.md §7 "Small-N latency").
+      cudaGraph_t g = nullptr;
+      LMS_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_eval(false);
+      } catch (...) {
+        cudaStreamEndCapture(stream_, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      LMS_CUDA(cudaStreamEndCapture(stream_, &g));
+      graph_launches_ = last_eval_launches;
+      cudaError_t e = cudaGraphInstantiate(&graph_, g, 0);
+      cudaGraphDestroy(g);
+      LMS_CUDA(e);
+    }
+  }
+  bound = true;
+}
+
+// Enqueue one objective evaluation on stream_: x (double, in d_x_) -> scalars in d_scalars_, grad in d_grad_.
+template <typename T, int D>
+void System<T, D>::enqueue_eval(bool timed)
+{
+  last_eval_launches = 0;
+  const int Tn = timesteps;
+  if (timed && (int)events_.size() < 4 * Tn) {
+    while ((int)events_.size() < 4 * Tn) {
+      cudaEvent_t e;
+      LMS_CUDA(cudaEventCreate(&e));
+      events_.push_back(e);
+    }
+  }
+  int ev = 0;
+  reset_diverged();
+  {
+    // p0[i][c] = T(x[i*D+c])  (registration.cpp:61-63); non-finite p0 -> DivergedError(0) (shooting.hpp:185-186)
+    const long long elems = (long long)n() * D;
+    aos_to_planes<T><<<ceil_div(elems, 256), 256, 0, stream_>>>(d_x_, snapshot(0) + D * stride_, stride_, n(), D,
+                                                                d_diverged_, 0);
+    LMS_CUDA(cudaGetLastError());
+    ++last_eval_launches;
+  }
+  // forward Euler flow, T+1 snapshots kept for the adjoint (shooting.hpp:199-212)
+  for (int t = 0; t < Tn; ++t) {
+    PairArgs<T> a = base_args();
+    a.jstate = a.istate = snapshot(t);
+    a.out = snapshot(t + 1);
+    a.adj_seed = adj_[0];
+    a.row_tile0 = row_tile_begin_(plan_fwd_.bm);
+    a.epi = kEpiEuler | (t == 0 ? kEpiFirstStep : 0u) | (t == Tn - 1 ? kEpiLastStep : 0u);
+    a.step = t + 1;
+    if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
+    launch<kFwd>(k_fwd_, a, plan_fwd_);
+    if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
+    if (world_ > 1) {
+      all_gather_state(snapshot(t + 1));
+      if (t == Tn - 1) all_gather_state(adj_[0]);
+    }
+  }
+  if (world_ > 1) {
+    all_gather_doubles(h_part_);
+    all_gather_doubles(mm_part_);
+  }
+  finalize_scalars<0><<<1, 32, 0, stream_>>>(h_part_, mm_part_, part_tiles_, lambda, d_scalars_);
+  LMS_CUDA(cudaGetLastError());
+  ++last_eval_launches;
+  // discrete adjoint sweep t = T-1 .. 0 (shooting.hpp:300-307), final gradient fused into the t = 0 launch
+  int cur = 0;
+  for (int t = Tn - 1; t >= 0; --t) {
+    PairArgs<T> a = base_args();
+    a.jstate = a.istate = snapshot(t);
+    a.jadj = a.iadj = adj_[cur];
+    a.out = adj_[cur ^ 1];
+    a.row_tile0 = row_tile_begin_(plan_adj_.bm);
+    a.epi = kEpiEuler | (t == 0 ? kEpiGradOut : 0u);
+    a.step = t;
+    if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
+    launch<kAdj>(k_adj_, a, plan_adj_);
+    if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
+    if (world_ > 1 && t > 0) all_gather_state(adj_[cur ^ 1]);
+    cur ^= 1;
+  }
+  if (world_ > 1) {
+    // every rank ends with the full gradient (row-major double rows are contiguous per rank slice)
+    const NcclApi& nc = nccl_api();
+    const size_t slice = (size_t)(stride_ / world_) * D;
+    if (nc.AllGather(d_grad_ + rank_ * slice, d_grad_, slice, kNcclFloat64, comm_, stream_) != 0)
+      throw StatusError{LMS_ERR_COMM, "ncclAllGather(grad) failed"};
+  }
+  final_adj_ = cur;
+}
+
+template <typename T, int D>
+void System<T, D>::eval(const double* x, double* grad, double* scalars, bool device_ptrs)
+{
+  if (!bound) throw StatusError{LMS_ERR_STATE, "lms_bind_registration must precede evaluation"};
+  if (n() == 0) {
+    scalars[0] = scalars[1] = scalars[2] = 0.0;
+    return;
+  }
+  if (q0_bad_) {
+    last_diverged_step = 0;
+    last_diverged_point = -1;
+    throw StatusError{LMS_ERR_DIVERGED, "non-finite template landmarks"};
+  }
+  const size_t bytes = (size_t)n() * D * sizeof(double);
+  if (!traj0_is_q0_) {
+    const long long elems = (long long)n() * D;
+    copy_planes<T><<<ceil_div(elems, 256), 256, 0, stream_>>>(q0_, stride_, snapshot(0), stride_, n(), D);
+    LMS_CUDA(cudaGetLastError());
+    traj0_is_q0_ = true;
+  }
+  LMS_CUDA(cudaMemcpyAsync(d_x_, x, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           stream_));
+  LMS_CUDA(cudaEventRecord(ev_begin_, stream_));
+  const bool timed = kernel_timing;
+  if (graph_ && !timed) {
+    LMS_CUDA(cudaGraphLaunch(graph_, stream_));
+    last_eval_launches = graph_launches_;
+  } else {
+    enqueue_eval(timed);
+  }
+  LMS_CUDA(cudaEventRecord(ev_end_, stream_));
+  LMS_CUDA(cudaMemcpyAsync(grad, d_grad_, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           stream_));
+  stored_t_ = timesteps;
+  read_diverged_or_throw();  // synchronises
+  float ms = 0.f;
+  LMS_CUDA(cudaEventElapsedTime(&ms, ev_begin_, ev_end_));
+  last_eval_ms = ms;
+  if (timed) {
+    double sum[2] = {0, 0};
+    for (int k = 0; k < 2 * timesteps; ++k) {
+      float m = 0.f;
+      LMS_CUDA(cudaEventElapsedTime(&m, events_[2 * k], events_[2 * k + 1]));
+      sum[k < timesteps ? 0 : 1] += m;
+    }
+    last_kernel_ms[0] = sum[0] / timesteps;
+    last_kernel_ms[1] = sum[1] / timesteps;
+  }
+  scalars[0] = h_scalars_[0];
+  scalars[1] = h_scalars_[1];
+  scalars[2] = h_scalars_[2];
+}
+
+template <typename T, int D>
+void System<T, D>::final_q(double* out)
+{
+  if (stored_t_ < 0) throw StatusError{LMS_ERR_STATE, "no stored trajectory"};
+  if (n() == 0) return;
+  download(snapshot(stored_t_), stride_, out, n(), D);
+  sync();
+}
+
+// ---- flow --------------------------------------------------------------------------------------------------------
+template <typename T, int D>
+void System<T, D>::ensure_points(size_t m)
+{
+  const long long need = std::max<long long>(round_up((long long)m, kRowAlign), kRowAlign);
+  if ((size_t)need > points_cap_) {
+    sync();
+    dev_free(points_[0]);
+    dev_free(points_[1]);
+    points_[0] = dev_alloc_zero<T>((size_t)need * D);
+    points_[1] = dev_alloc_zero<T>((size_t)need * D);
+    points_cap_ = (size_t)need;
+  }
+  points_stride_ = (long long)points_cap_;
+}
+
+template <typename T, int D>
+void System<T, D>::velocities(const double* q, const double* p, size_t m, const double* pts, double* out)
+{
+  if (m == 0) return;
+  ensure_points(m);
+  if (n() > 0) {
+    upload(q, scratch_in_, stride_, n(), D, false, 0);
+    upload(p, scratch_in_ + D * stride_, stride_, n(), D, false, 0);
+  }
+  upload(pts, points_[0], points_stride_, (int)m, D, false, 0);
+  if (n() == 0) {  // empty sum
+    std::fill(out, out + m * D, 0.0);
+    sync();
+    return;
+  }
+  LaunchPlan plan = plan_for<kVel>(k_vel_, (int)m);
+  ensure_partials(plan.partial_elems, plan.n_row_tiles);
+  PairArgs<T> a = base_args();
+  a.jstate = scratch_in_;
+  a.istate = points_[0];
+  a.istride = points_stride_;
+  a.n_rows = (int)m;
+  a.out = points_[1];
+  a.ostride = points_stride_;
+  launch<kVel>(k_vel_, a, plan);
+  download(points_[1], points_stride_, out, (int)m, D);
+  sync();
+}
+
+template <typename T, int D>
+void System<T, D>::warp_stored(size_t m, const double* pts, double* out)
+{
+  if (stored_t_ < 1) throw StatusError{LMS_ERR_STATE, "no stored trajectory: integrate or evaluate first"};
+  if (m == 0) return;
+  ensure_points(m);
+  reset_diverged();
+  upload(pts, points_[0], points_stride_, (int)m, D, false, 0);
+  int cur = 0;
+  if (n() > 0) {
+    LaunchPlan plan = plan_for<kVel>(k_vel_, (int)m);
+    ensure_partials(plan.partial_elems, plan.n_row_tiles);
+    const T dt = T(1.0 / stored_t_);  // the trajectory's own dt (flow.hpp:70)
+    for (int t = 0; t < stored_t_; ++t) {
+      PairArgs<T> a = base_args();
+      a.jstate = snapshot(t);
+      a.istate = points_[cur];
+      a.istride = points_stride_;
+      a.n_rows = (int)m;
+      a.out = points_[cur ^ 1];
+      a.ostride = points_stride_;
+      a.dt = dt;
+      a.epi = kEpiEuler;
+      a.step = t + 1;
+      launch<kVel>(k_vel_, a, plan);
+      cur ^= 1;
+    }
+  }
+  read_diverged_or_throw();
+  download(points_[cur], points_stride_, out, (int)m, D);
+  sync();
+}
+
+// ---- row partition over NCCL ------------------------------------------------------------------------------------------
+template <typename T, int D>
+void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
+{
+  if (world < 1 || rank < 0 || rank >= world) throw StatusError{LMS_ERR_INVALID, "bad rank/world"};
+  if (world == 1) return;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) throw StatusError{LMS_ERR_COMM, "libnccl.so.2 could not be loaded"};
+  sync();
+  destroy_graph();
+  bound = false;
+  // Re-lay the planes so that every rank owns an equal, tile-aligned slice (in-place all-gather).
+  const long long N = (long long)cfg.n;
+  const long long slice = std::max<long long>(round_up((N + world - 1) / world, kRowAlign), kRowAlign);
+  const long long new_stride = slice * world;
+  if (new_stride != stride_) {
+    stride_ = new_stride;
+    const size_t plane = (size_t)stride_;
+    dev_free(traj_); dev_free(adj_[0]); dev_free(adj_[1]); dev_free(hp0_); dev_free(target_); dev_free(q0_);
+    dev_free(scratch_in_); dev_free(scratch_out_); dev_free(d_x_); dev_free(d_grad_); dev_free(h_part_);
+    dev_free(mm_part_);
+    traj_ = dev_alloc_zero<T>((size_t)(max_t_ + 1) * kState * plane);
+    adj_[0] = dev_alloc_zero<T>(kState * plane);
+    adj_[1] = dev_alloc_zero<T>(kState * plane);
+    hp0_ = dev_alloc_zero<T>(D * plane);
+    target_ = dev_alloc_zero<T>(D * plane);
+    q0_ = dev_alloc_zero<T>(D * plane);
+    scratch_in_ = dev_alloc_zero<T>(2 * kState * plane);
+    scratch_out_ = dev_alloc_zero<T>(kState * plane);
+    d_x_ = dev_alloc_zero<double>(plane * D);
+    d_grad_ = dev_alloc_zero<double>(plane * D);
+    part_tiles_ = (int)(stride_ / kThreads);
+    h_part_ = dev_alloc_zero<double>(part_tiles_);
+    mm_part_ = dev_alloc_zero<double>(part_tiles_);
+  }
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, sizeof(uid.internal));
+  if (nc.CommInitRank(&comm_, world, uid, rank) != 0) throw StatusError{LMS_ERR_COMM, "ncclCommInitRank failed"};
+  rank_ = rank;
+  world_ = world;
+}
+
+// In-place all-gather of every plane of a (q,p) or (alpha,beta) state: rank r contributes rows
+// [r*slice, (r+1)*slice) of each plane.
+template <typename T, int D>
+void System<T, D>::all_gather_state(T* planes)
+{
+  const NcclApi& nc = nccl_api();
+  const size_t slice = (size_t)(stride_ / world_);
+  const int dtype = sizeof(T) == 4 ? kNcclFloat32 : kNcclFloat64;
+  bool ok = nc.GroupStart() == 0;
+  for (int k = 0; k < kState && ok; ++k) {
+    T* plane = planes + (long long)k * stride_;
+    ok = nc.AllGather(plane + rank_ * slice, plane, slice, dtype, comm_, stream_) == 0;
+  }
+  ok = (nc.GroupEnd() == 0) && ok;
+  if (!ok) throw StatusError{LMS_ERR_COMM, "ncclAllGather(state) failed"};
+}
+
+// Per-row-tile double partials: tiles are indexed globally, each rank filled its own contiguous range.
+template <typename T, int D>
+void System<T, D>::all_gather_doubles(double* buf)
+{
+  const NcclApi& nc = nccl_api();
+  const size_t slice = (size_t)(part_tiles_ / world_);
+  if (nc.AllGather(buf + rank_ * slice, buf, slice, kNcclFloat64, comm_, stream_) != 0)
+    throw StatusError{LMS_ERR_COMM, "ncclAllGather(partials) failed"};
+}
+
+const char* variant_name(int precision, int variant)
+{
+  // names of the 3-D forward kernels; the adjoint / velocity variants follow the same index
+  if (precision == LMS_PRECISION_F32) return pick_kernel<float, 3, kFwd>(variant).name;
+  return pick_kernel<double, 3, kFwd>(variant).name;
+}
+
+SystemBase* create_system(const lms_config& cfg)
+{
+  const bool f32 = cfg.precision == LMS_PRECISION_F32;
+  if (cfg.dim == 3) return f32 ? (SystemBase*)new System<float, 3>(cfg) : (SystemBase*)new System<double, 3>(cfg);
+  return f32 ? (SystemBase*)new System<float, 2>(cfg) : (SystemBase*)new System<double, 2>(cfg);
+}
+
+}  // namespace lms

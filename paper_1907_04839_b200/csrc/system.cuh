@@ -1,0 +1,203 @@
+// Host-side engine behind the C ABI: device-resident state, launch plans, the evaluation graph.
+// Mirrors HamiltonianSystem<T,D> (shooting.hpp:104-344) and the objective closure
+// (registration.cpp:58-74); see include/lmshoot_b200.h for the per-call citations.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/lmshoot_b200.h"
+#include "nccl_dyn.h"
+#include "pair_kernels.cuh"
+
+namespace lms {
+
+struct CudaFailure {
+  cudaError_t err;
+  const char* what;
+  int line;
+};
+
+#define LMS_CUDA(expr)                                          \
+  do {                                                          \
+    cudaError_t lms_e_ = (expr);                                \
+    if (lms_e_ != cudaSuccess) throw CudaFailure{lms_e_, #expr, __LINE__}; \
+  } while (0)
+
+struct StatusError {
+  int code;
+  const char* msg;
+};
+
+constexpr unsigned long long kNotDiverged = ~0ull;
+constexpr int kRowAlign = 512;  // planes are padded to a multiple of the largest row tile
+
+// Abstract interface the C ABI talks to (one concrete System<T,D> per precision x dim).
+class SystemBase {
+ public:
+  virtual ~SystemBase() = default;
+  virtual void hamiltonian(const double* q, const double* p, double* out) = 0;
+  virtual void derivatives(const double* q, const double* p, double* hq, double* hp) = 0;
+  virtual void integrate_forward(const double* q0, const double* p0, int timesteps, double* tq, double* tp) = 0;
+  virtual void adjoint_step(const double* q, const double* p, const double* alpha, const double* beta,
+                            double* da, double* db) = 0;
+  virtual void mismatch_sq(const double* a, const double* b, double* out) = 0;
+  virtual void bind(const double* q0, const double* target, double lambda, int timesteps) = 0;
+  virtual void eval(const double* x, double* grad, double* scalars, bool device_ptrs) = 0;
+  virtual void final_q(double* out) = 0;
+  virtual void velocities(const double* q, const double* p, size_t m, const double* pts, double* out) = 0;
+  virtual void warp_stored(size_t m, const double* pts, double* out) = 0;
+  virtual void comm_init(const unsigned char* id, int rank, int world) = 0;
+
+  lms_config cfg{};
+  int last_diverged_step = -1;
+  long long last_diverged_point = -1;
+  std::string last_message;
+  double last_eval_ms = 0.0;
+  int last_eval_launches = 0;
+  bool kernel_timing = false;
+  double last_kernel_ms[2] = {0.0, 0.0};
+  // bound registration (host copies feed lms_register's x0 = (target - q0)/T, registration.cpp:47-52)
+  bool bound = false;
+  std::vector<double> host_q0, host_target;
+  double lambda = 0.0;
+  int timesteps = 0;
+};
+
+// ---- kernel variants --------------------------------------------------------------------------
+template <typename T>
+struct KernelChoice {
+  void (*fn)(PairArgs<T>) = nullptr;
+  int rows_per_thread = 0;
+  const char* name = "";
+};
+
+template <typename T, int D, int MODE, int R, int JU, int MINB>
+KernelChoice<T> make_choice(const char* name)
+{
+  KernelChoice<T> c;
+  c.fn = pair_kernel<T, D, MODE, R, JU, MINB>;
+  c.rows_per_thread = R;
+  c.name = name;
+  return c;
+}
+
+// variant 0 is the library default; the others exist so one GPU session can A/B them.
+template <typename T, int D, int MODE>
+KernelChoice<T> pick_kernel(int variant);
+
+struct LaunchPlan {
+  int grid = 0;
+  int max_seg = 1;
+  int n_row_tiles = 0;
+  int n_j_tiles = 0;
+  int bm = 0;
+  size_t partial_elems = 0;
+};
+
+template <typename T, int D>
+class System final : public SystemBase {
+ public:
+  explicit System(const lms_config& c);
+  ~System() override;
+
+  void hamiltonian(const double* q, const double* p, double* out) override;
+  void derivatives(const double* q, const double* p, double* hq, double* hp) override;
+  void integrate_forward(const double* q0, const double* p0, int timesteps, double* tq, double* tp) override;
+  void adjoint_step(const double* q, const double* p, const double* alpha, const double* beta, double* da,
+                    double* db) override;
+  void mismatch_sq(const double* a, const double* b, double* out) override;
+  void bind(const double* q0, const double* target, double lambda, int timesteps) override;
+  void eval(const double* x, double* grad, double* scalars, bool device_ptrs) override;
+  void final_q(double* out) override;
+  void velocities(const double* q, const double* p, size_t m, const double* pts, double* out) override;
+  void warp_stored(size_t m, const double* pts, double* out) override;
+  void comm_init(const unsigned char* id, int rank, int world) override;
+
+ private:
+  static constexpr int kState = 2 * D;  // planes per (q,p) or (alpha,beta) state
+
+  T* snapshot(int t) const { return traj_ + (long long)t * kState * stride_; }
+  int n() const { return (int)cfg.n; }
+
+  template <int MODE>
+  LaunchPlan plan_for(const KernelChoice<T>& k, int n_rows, int row_tile0 = -1, int row_tiles = -1);
+  template <int MODE>
+  void launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchPlan& plan);
+  void ensure_partials(size_t elems, int row_tiles);
+  PairArgs<T> base_args() const;
+
+  void upload(const double* host, T* planes, long long stride, int count, int ncomp, bool check, int step);
+  void download(const T* planes, long long stride, double* host, int count, int ncomp);
+  void reset_diverged();
+  void read_diverged_or_throw();
+  void sync() { LMS_CUDA(cudaStreamSynchronize(stream_)); }
+  void enqueue_eval(bool timed);
+  void destroy_graph();
+  void ensure_points(size_t m);
+  void all_gather_state(T* state_planes);
+  void all_gather_doubles(double* buf);
+
+  cudaStream_t stream_ = nullptr;
+  int num_sms_ = 0;
+  long long stride_ = 0;
+  int max_t_ = 0;
+  T inv_sig2_{}, kexp_{};
+
+  KernelChoice<T> k_fwd_, k_adj_, k_vel_;
+
+  T* traj_ = nullptr;
+  T* adj_[2] = {nullptr, nullptr};
+  T* hp0_ = nullptr;
+  T* target_ = nullptr;
+  T* q0_ = nullptr;
+  T* scratch_in_ = nullptr;
+  T* scratch_out_ = nullptr;
+  T* points_[2] = {nullptr, nullptr};
+  size_t points_cap_ = 0;
+  long long points_stride_ = 0;
+  T* partials_ = nullptr;
+  size_t partials_cap_ = 0;
+  int* counters_ = nullptr;
+  int counters_cap_ = 0;
+  double* h_part_ = nullptr;
+  double* mm_part_ = nullptr;
+  int part_tiles_ = 0;
+  double* d_scalars_ = nullptr;
+  unsigned long long* d_diverged_ = nullptr;
+  double* d_io_ = nullptr;  // 4 x (n*D) doubles of conversion staging
+  double* d_x_ = nullptr;
+  double* d_grad_ = nullptr;
+  double* h_scalars_ = nullptr;  // pinned: 3 doubles + the divergence word
+  size_t io_cap_ = 0;
+
+  // bound problem
+  T dt_{}, two_lambda_{};
+  bool q0_bad_ = false;
+  bool traj0_is_q0_ = false;
+  int stored_t_ = -1;  // timesteps of the trajectory currently in traj_ (-1: none)
+  int final_adj_ = 0;  // which adj_ buffer holds (alpha_0, beta_0) after an eval
+  LaunchPlan plan_fwd_, plan_adj_;
+  cudaGraphExec_t graph_ = nullptr;
+  int graph_launches_ = 0;
+  std::vector<cudaEvent_t> events_;
+  cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr;
+
+  // row partition (multi-GPU)
+  int rank_ = 0, world_ = 1;
+  ncclComm_t comm_ = nullptr;
+  int row_tile_begin_(int bm) const;
+  int row_tile_end_(int bm) const;
+};
+
+SystemBase* create_system(const lms_config& cfg);
+const char* variant_name(int precision, int variant);
+
+}  // namespace lms

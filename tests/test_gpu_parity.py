@@ -1,0 +1,395 @@
+"""GPU parity tests proper: the CUDA path, called through the C ABI (ctypes -> liblmshoot_b200.so),
+against the CPU oracle on the same seeded inputs, against the committed golden fixtures, and -- at
+BASELINE.json's full sizes -- through row subsets and size-independent properties.
+
+Tolerances (BASELINE.json north_star / BASELINE.md §4): loss, H and ||dg||_inf/||g||_inf per evaluation
+within 1e-10 in fp64 and 1e-5 in fp32 (at well-conditioned evaluation points); integer/index results and
+the strictly sequential double sums are bit-exact."""
+import numpy as np
+import pytest
+
+from conftest import rel_inf, synth_case
+
+pytestmark = pytest.mark.gpu
+
+SIGMA = 1.5
+TOL = {"f64": 1e-10, "f32": 1e-5}
+EDGE_N = [1, 2, 7, 255, 256, 257, 513, 1000]
+
+
+@pytest.fixture(scope="module")
+def hs():
+    from paper_1907_04839_b200 import HamiltonianSystem
+
+    cache = {}
+
+    def make(n, dim, prec, max_t=40, variant=0):
+        key = (n, dim, prec, max_t, variant)
+        if key not in cache:
+            cache[key] = HamiltonianSystem(SIGMA, n, dim, prec, device=0, max_timesteps=max_t, variant=variant)
+        return cache[key]
+
+    yield make
+    for s in cache.values():
+        s.close()
+
+
+def test_extension_is_loaded_and_runs_on_device(hs):
+    import ctypes
+
+    from paper_1907_04839_b200 import _lib
+
+    assert isinstance(_lib.load(), ctypes.CDLL)
+    s = hs(64, 3, "f32")
+    q, p, target, *_ = synth_case(64, 3, 1)
+    s.compute_gradient(q, p, target, 10.0, 4)
+    assert s.last_eval_kernel_launches() == 2 * 4 + 2
+    assert s.last_eval_device_ms() > 0.0
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("n", [1, 2, 7, 33, 200])
+def test_against_golden_fixtures(hs, golden_hotpath, prec, dim, n):
+    g, k, tol = golden_hotpath, f"{prec}_d{dim}_n{n}_", TOL[prec]
+    q, p, target, alpha, beta, pts = (g[k + s] for s in ("q", "p", "target", "alpha", "beta", "pts"))
+    s = hs(n, dim, prec)
+    hq, hp = s.derivatives(q, p)
+    assert rel_inf(hq, g[k + "hq"]) <= tol and rel_inf(hp, g[k + "hp"]) <= tol
+    assert s.hamiltonian(q, p) == pytest.approx(float(g[k + "H"]), rel=tol)
+    da, db = s.adjoint_step(q, p, alpha, beta)
+    assert rel_inf(da, g[k + "dalpha"]) <= tol and rel_inf(db, g[k + "dbeta"]) <= tol
+    assert s.mismatch_sq(q, target) == float(g[k + "mismatch"])  # sequential double sum: bit-exact
+    tq, tp = s.integrate_forward(q, p, 4)
+    assert rel_inf(tq, g[k + "traj_q"]) <= tol and rel_inf(tp, g[k + "traj_p"]) <= tol
+    assert np.array_equal(tq[0], g[k + "traj_q"][0])  # snapshot 0 is the input cast to T, exactly
+    assert rel_inf(s.warp_points(pts), g[k + "warped"]) <= tol
+    assert rel_inf(s.velocities_at_step(q, p, pts), g[k + "vel"]) <= tol
+    r = s.compute_gradient(q, p, target, 10.0, 4)
+    want = g[k + "scalars"]
+    assert r.loss == pytest.approx(want[0], rel=tol) and r.kinetic == pytest.approx(want[1], rel=tol)
+    assert r.mismatch == pytest.approx(want[2], rel=tol)
+    assert rel_inf(r.grad, g[k + "grad"]) <= tol
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("n", EDGE_N)
+def test_per_function_parity_vs_oracle(hs, oracle, prec, n):
+    """Tile-boundary sizes (255/256/257 straddle the 128-column tile and the 256/512-row tiles)."""
+    tol = TOL[prec]
+    q, p, target, alpha, beta = synth_case(n, 3, 100 + n, spread=6.0)
+    s = hs(n, 3, prec)
+    hq, hp = s.derivatives(q, p)
+    ohq, ohp = oracle.derivatives(prec, q, p, SIGMA)
+    assert rel_inf(hq, ohq) <= tol and rel_inf(hp, ohp) <= tol
+    da, db = s.adjoint_step(q, p, alpha, beta)
+    oda, odb = oracle.adjoint_step(prec, q, p, alpha, beta, SIGMA)
+    assert rel_inf(da, oda) <= tol and rel_inf(db, odb) <= tol
+    assert s.hamiltonian(q, p) == pytest.approx(oracle.hamiltonian(prec, q, p, SIGMA), rel=tol)
+    assert s.mismatch_sq(q, target) == oracle.mismatch_sq(prec, q, target)
+    tq, tp = s.integrate_forward(q, p, 10)
+    otq, otp = oracle.integrate_forward(prec, q, p, SIGMA, 10)
+    assert rel_inf(tq, otq) <= tol and rel_inf(tp, otp) <= tol
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("n,T,lam", [(1, 1, 3.0), (2, 5, 10.0), (7, 10, 10.0), (257, 10, 10.0), (1000, 10, 10.0),
+                                     (1000, 10, 5e5), (600, 40, 5e5)])
+def test_compute_gradient_parity(hs, oracle, prec, n, T, lam):
+    tol = TOL[prec]
+    q, p, target, *_ = synth_case(n, 3, 200 + n + T, spread=8.0)
+    s = hs(n, 3, prec)
+    r = s.compute_gradient(q, p, target, lam, T)
+    loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, SIGMA, lam, T)
+    assert r.loss == pytest.approx(loss, rel=tol)
+    assert r.kinetic == pytest.approx(kin, rel=tol)
+    assert r.mismatch == pytest.approx(mm, rel=tol)
+    assert rel_inf(r.grad, grad) <= tol
+    assert rel_inf(s.final_q(), oracle.integrate_forward(prec, q, p, SIGMA, T)[0][-1]) <= tol
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_two_dimensional_landmarks(hs, oracle, prec):
+    tol = TOL[prec]
+    q, p, target, alpha, beta = synth_case(300, 2, 7, spread=5.0)
+    s = hs(300, 2, prec)
+    r = s.compute_gradient(q, p, target, 10.0, 6)
+    loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, SIGMA, 10.0, 6)
+    assert r.loss == pytest.approx(loss, rel=tol) and rel_inf(r.grad, grad) <= tol
+    da, db = s.adjoint_step(q, p, alpha, beta)
+    oda, odb = oracle.adjoint_step(prec, q, p, alpha, beta, SIGMA)
+    assert rel_inf(da, oda) <= tol and rel_inf(db, odb) <= tol
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("variant", [1, 2, 3])
+def test_kernel_variants_agree_with_oracle(hs, oracle, prec, variant):
+    tol = TOL[prec]
+    n = 700
+    q, p, target, *_ = synth_case(n, 3, 300 + variant, spread=7.0)
+    s = hs(n, 3, prec, variant=variant)
+    r = s.compute_gradient(q, p, target, 10.0, 5)
+    loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, SIGMA, 10.0, 5)
+    assert r.loss == pytest.approx(loss, rel=tol) and rel_inf(r.grad, grad) <= tol
+
+
+def test_known_answers_through_the_abi(hs):
+    """SPEC.md:158-216 closed forms, fp64."""
+    s1 = hs(1, 3, "f64")
+    q, p = np.array([[0.3, -1.0, 2.0]]), np.array([[1.0, 0.5, -0.25]])
+    assert s1.hamiltonian([[0, 0, 0]], [[1, 0, 0]]) == 0.5
+    hq, hp = s1.derivatives(q, p)
+    assert np.array_equal(hp, p) and np.array_equal(hq, np.zeros_like(q))
+    tq, _ = s1.integrate_forward([[0, 0, 0]], [[1, 0, 0]], 8)
+    assert np.allclose(tq[-1], [[1.0, 0, 0]], rtol=0, atol=1e-15)
+    alpha, beta = np.array([[0.2, 0.1, -0.4]]), np.array([[1.0, 2.0, 3.0]])
+    da, db = s1.adjoint_step(q, p, alpha, beta)
+    assert np.array_equal(da, np.zeros_like(q)) and np.array_equal(db, alpha)
+    target, lam = np.array([[1.0, 1.0, 1.0]]), 3.0
+    r = s1.compute_gradient(q, p, target, lam, 1)
+    assert np.allclose(r.grad, p + 2 * lam * (q + p - target), rtol=1e-15)
+    s2 = hs(2, 3, "f64")
+    h = s2.hamiltonian([[0, 0, 0], [1.5, 0, 0]], [[1, 0, 0], [1, 0, 0]])
+    assert h == pytest.approx(1 + np.exp(-0.5), rel=1e-14)
+    q6, _, t6, *_ = synth_case(6, 3, 11)
+    s6 = hs(6, 3, "f64")
+    r = s6.compute_gradient(q6, np.zeros_like(q6), q6, 7.0, 3)
+    assert r.loss == 0.0 and not r.grad.any()
+    r = s6.compute_gradient(q6, np.zeros_like(q6), t6, 7.0, 3)
+    assert r.kinetic == 0.0 and r.loss == pytest.approx(7.0 * float(((q6 - t6) ** 2).sum()), rel=1e-14)
+
+
+def test_gradient_vs_finite_differences_on_device(hs):
+    """the device gradient is the exact gradient of the device's own discrete loss."""
+    n, T, lam = 20, 10, 10.0
+    q, p, target, *_ = synth_case(n, 3, 61, spread=2.0)
+    s = hs(n, 3, "f64")
+    grad = s.compute_gradient(q, p, target, lam, T).grad
+    s.bind_registration(q, target, lam, T)
+    eps = 1e-5
+    fd = np.zeros_like(p)
+    for idx in np.ndindex(*p.shape):
+        orig = p[idx]
+        p[idx] = orig + eps
+        hi, _ = s.objective(p)
+        p[idx] = orig - eps
+        lo, _ = s.objective(p)
+        p[idx] = orig
+        fd[idx] = (hi - lo) / (2 * eps)
+    assert rel_inf(fd, grad) <= 1e-6
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_bitwise_run_to_run_determinism(hs, prec):
+    n = 3000
+    q, p, target, *_ = synth_case(n, 3, 5, spread=10.0)
+    s = hs(n, 3, prec)
+    s.bind_registration(q, target, 5e5, 10)
+    first = s.objective(p)
+    for _ in range(3):
+        again = s.objective(p)
+        assert again[0] == first[0] and np.array_equal(again[1], first[1])
+    # a fresh handle (new buffers, new graph) gives the same bits too
+    from paper_1907_04839_b200 import HamiltonianSystem
+
+    other = HamiltonianSystem(SIGMA, n, 3, prec, max_timesteps=10)
+    other.bind_registration(q, target, 5e5, 10)
+    fresh = other.objective(p)
+    other.close()
+    assert fresh[0] == first[0] and np.array_equal(fresh[1], first[1])
+
+
+def test_divergence_semantics(hs, oracle):
+    from oracle.binding import OracleError
+    from paper_1907_04839_b200 import DivergedError
+
+    n = 40
+    q, p, target, *_ = synth_case(n, 3, 8)
+    s = hs(n, 3, "f32")
+    bad = p.copy()
+    bad[3, 1] = np.nan
+    with pytest.raises(DivergedError) as e:
+        s.integrate_forward(q, bad, 5)
+    assert e.value.timestep == 0  # shooting.hpp:185-186
+    with pytest.raises(DivergedError) as e:
+        s.compute_gradient(q, bad, target, 1.0, 5)
+    assert e.value.timestep == 0
+    bad_q = q.copy()
+    bad_q[0, 0] = np.inf
+    with pytest.raises(DivergedError) as e:
+        s.compute_gradient(bad_q, p, target, 1.0, 5)
+    assert e.value.timestep == 0
+    # overflow part-way: the reported step equals the reference's first non-finite step (:210-211)
+    huge = p.copy()
+    huge[0, 0] = 1e30
+    with pytest.raises(OracleError) as want:
+        oracle.integrate_forward("f32", q * 1e18, huge, SIGMA, 6)
+    with pytest.raises(DivergedError) as got:
+        s.integrate_forward(q * 1e18, huge, 6)
+    assert got.value.timestep == want.value.timestep >= 1
+    # the handle stays usable after an error
+    r = s.compute_gradient(q, p, target, 1.0, 5)
+    assert np.isfinite(r.loss)
+
+
+def test_shape_and_state_errors(hs):
+    from paper_1907_04839_b200 import HamiltonianSystem, ShapeError, StateError
+
+    s = hs(10, 3, "f64")
+    q, p, *_ = synth_case(10, 3, 1)
+    with pytest.raises(ShapeError):
+        s.derivatives(q, p[:9])  # require_same, shooting.hpp:332-338
+    with pytest.raises(ShapeError):
+        s.derivatives(q[:, :2], p[:, :2])
+    with pytest.raises(ValueError):
+        s.integrate_forward(q, p, 0)  # shooting.hpp:184
+    with pytest.raises(ValueError):
+        s.integrate_forward(q, p, 41)  # beyond the handle's trajectory capacity
+    fresh = HamiltonianSystem(SIGMA, 10, 3, "f64", max_timesteps=4)
+    with pytest.raises(StateError):
+        fresh.objective(p)
+    with pytest.raises(StateError):
+        fresh.warp_points(q)
+    fresh.close()
+
+
+def test_empty_problem(hs):
+    s = hs(0, 3, "f64")
+    z = np.zeros((0, 3))
+    r = s.compute_gradient(z, z, z, 1.0, 2)
+    assert (r.loss, r.kinetic, r.mismatch) == (0.0, 0.0, 0.0) and r.grad.shape == (0, 3)
+    assert s.hamiltonian(z, z) == 0.0
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_flow_velocities_and_warp(hs, oracle, prec):
+    tol = TOL[prec]
+    n, m, T = 500, 1300, 10
+    q, p, *_ = synth_case(n, 3, 17, spread=6.0)
+    pts = np.random.default_rng(3).uniform(-7, 7, (m, 3))
+    s = hs(n, 3, prec)
+    assert rel_inf(s.velocities_at_step(q, p, pts), oracle.velocities(prec, q, p, pts, SIGMA)) <= tol
+    tq, tp = s.integrate_forward(q, p, T)
+    otq, otp = oracle.integrate_forward(prec, q, p, SIGMA, T)
+    assert rel_inf(s.warp_points(pts), oracle.warp_points(prec, otq, otp, pts, SIGMA)) <= tol
+    # warping the template itself reproduces q(T)
+    assert rel_inf(s.warp_points(q), tq[-1]) <= tol
+
+
+# ---- full-size checks (BASELINE.json configs[1]: N = 20 000, T = 10) ---------------------------------------
+@pytest.fixture(scope="module")
+def full_case():
+    from paper_1907_04839_b200 import make_synthetic_pair
+
+    n, T = 20000, 10
+    q0, target, p_true = make_synthetic_pair(n, SIGMA, T)
+    x0 = (target - q0) / T  # paper initialisation, registration.cpp:47-52
+    return n, T, q0, target, p_true, x0
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_full_size_row_subset_parity(hs, oracle, full_case, prec):
+    """N = 20 000: 96 rows of derivatives and adjoint_step against the oracle's identical per-row sums."""
+    n, T, q0, target, p_true, x0 = full_case
+    tol = TOL[prec]
+    rows = np.unique(np.concatenate([[0, 1, 127, 128, 511, 512, n - 1], np.random.default_rng(9).integers(0, n, 89)]))
+    s = hs(n, 3, prec, max_t=T)
+    hq, hp = s.derivatives(q0, p_true)
+    ohq, ohp = oracle.pair_rows(prec, q0, p_true, rows, SIGMA)
+    scale_q, scale_p = np.abs(hq).max(), np.abs(hp).max()
+    assert np.abs(hq[rows] - ohq).max() <= tol * scale_q and np.abs(hp[rows] - ohp).max() <= tol * scale_p
+    rng = np.random.default_rng(10)
+    alpha, beta = rng.normal(size=(n, 3)), rng.normal(size=(n, 3))
+    da, db = s.adjoint_step(q0, p_true, alpha, beta)
+    oda, odb = oracle.pair_rows(prec, q0, p_true, rows, SIGMA, alpha, beta)
+    assert np.abs(da[rows] - oda).max() <= tol * np.abs(da).max()
+    assert np.abs(db[rows] - odb).max() <= tol * np.abs(db).max()
+
+
+def test_full_size_properties_fp64(hs, full_case):
+    """Size-independent properties at N = 20 000."""
+    n, T, q0, target, p_true, x0 = full_case
+    s = hs(n, 3, "f64", max_t=T)
+    # the synthetic target is reachable: shooting with the true momenta lands on it exactly
+    tq, tp = s.integrate_forward(q0, p_true, T)
+    assert np.array_equal(tq[-1], target)
+    # total momentum is conserved by the Euler flow
+    drift = np.abs(tp.sum(axis=1) - p_true.sum(axis=0)).max()
+    assert drift <= 1e-10 * np.linalg.norm(p_true, axis=1).sum()
+    # translation invariance of H, and H = 1/2 sum p.hp
+    h = s.hamiltonian(q0, p_true)
+    assert s.hamiltonian(q0 + np.array([3.0, -2.0, 5.0]), p_true) == pytest.approx(h, rel=1e-12)
+    hq, hp = s.derivatives(q0, p_true)
+    assert 0.5 * float((p_true * hp).sum()) == pytest.approx(h, rel=1e-12)
+    assert np.abs(hq.sum(axis=0)).max() <= 1e-9 * np.abs(hq).sum()
+    # gradient: at p_true the mismatch vanishes, so grad = hp(q0, p_true) and loss = H
+    s.bind_registration(q0, target, 5e5, T)
+    loss, grad = s.objective(p_true)
+    assert loss == pytest.approx(h, rel=1e-12)
+    assert rel_inf(grad.reshape(n, 3), hp) <= 1e-9
+    # directional finite difference of the discrete loss at the paper's initial point
+    rng = np.random.default_rng(4)
+    v = rng.normal(size=x0.shape)
+    v /= np.linalg.norm(v)
+    loss0, g0 = s.objective(x0)
+    eps = 1e-6
+    hi, _ = s.objective(x0 + eps * v)
+    lo, _ = s.objective(x0 - eps * v)
+    assert (hi - lo) / (2 * eps) == pytest.approx(float(g0 @ v.ravel()), rel=1e-6)
+    # permutation equivariance
+    perm = rng.permutation(n)
+    s.bind_registration(q0[perm], target[perm], 5e5, T)
+    loss_p, g_p = s.objective(x0[perm])
+    assert loss_p == pytest.approx(loss0, rel=1e-12)
+    assert rel_inf(g_p.reshape(n, 3), g0.reshape(n, 3)[perm]) <= 1e-10
+
+
+def test_full_size_fp32_tracks_fp64(hs, full_case):
+    """fp32 at N = 20 000 against the device's own fp64 result at the paper's initial point."""
+    n, T, q0, target, p_true, x0 = full_case
+    s64, s32 = hs(n, 3, "f64", max_t=T), hs(n, 3, "f32", max_t=T)
+    s64.bind_registration(q0, target, 5e5, T)
+    s32.bind_registration(q0, target, 5e5, T)
+    l64, g64 = s64.objective(x0)
+    l32, g32 = s32.objective(x0)
+    assert l32 == pytest.approx(l64, rel=1e-5)
+    assert s32.last_kinetic == pytest.approx(s64.last_kinetic, rel=1e-5)
+    assert rel_inf(g32, g64) <= 2e-5
+
+
+# ---- the optimiser end to end (BASELINE.json configs[0]) ----------------------------------------------------
+def test_small_registration_matches_reference_golden(golden_optimiser):
+    """The reference's own register run (oracle/_ref, committed fixture): 96 landmarks, 12 iterations."""
+    from paper_1907_04839_b200 import ShootingConfig, register_landmarks
+
+    g = golden_optimiser
+    sigma, lam, T, iters = g["reg_meta_sigma_lambda_T_iters"]
+    for prec, tol_mm in (("f64", 1e-6), ("f32", 5e-3)):
+        cfg = ShootingConfig(sigma=float(sigma), timesteps=int(T), lam=float(lam), max_iter=int(iters), precision=prec)
+        r = register_landmarks(g["reg_q0"], g["reg_target"], cfg)
+        want_loss, want_init, want_evals, want_iters, _ = g[f"reg_{prec}_summary"]
+        assert r.initial_loss == pytest.approx(want_init, rel=TOL[prec])
+        assert np.abs(r.warped - g[f"reg_{prec}_warped"]).max() <= tol_mm
+        if prec == "f64":
+            assert (r.evaluations, r.iterations) == (int(want_evals), int(want_iters))
+            assert r.final_loss == pytest.approx(want_loss, rel=1e-7)
+            assert np.allclose(r.hist_loss, g["reg_f64_hist_loss"], rtol=1e-7)
+
+
+def test_hundred_iteration_registration_n1000(oracle, reference):
+    """configs[0]: N = 1000, T = 10, 100 L-BFGS iterations; the reference CPU path runs it too.
+    Final matched landmarks within 1e-6 mm in fp64."""
+    from paper_1907_04839_b200 import ShootingConfig, make_synthetic_pair, register_landmarks
+
+    n, T, lam = 1000, 10, 5e5
+    q0, target, _ = make_synthetic_pair(n, SIGMA, T)
+    cfg = ShootingConfig(sigma=SIGMA, timesteps=T, lam=lam, max_iter=100, precision="f64")
+    got = register_landmarks(q0, target, cfg)
+    want = reference.register("f64", q0, target, SIGMA, lam, T, 100)
+    assert got.initial_loss == pytest.approx(want["initial_loss"], rel=1e-10)
+    assert np.abs(got.warped - want["warped"]).max() <= 1e-6
+    assert got.final_loss == pytest.approx(want["loss"], rel=1e-6)
+    assert got.avg_after < 1e-2 * got.avg_before
+    cfg32 = ShootingConfig(sigma=SIGMA, timesteps=T, lam=lam, max_iter=100, precision="f32")
+    got32 = register_landmarks(q0, target, cfg32)
+    assert np.abs(got32.warped - want["warped"]).max() <= 5e-3
