@@ -131,7 +131,7 @@ def cpu_reference_run(n_sample, timesteps, precision, steps, warmup):
     i = np.arange(n_sample, dtype=np.float64)
     z = 1.0 - 2.0 * (i + 0.5) / n_sample
     r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
-    radius = 20.0 * np.sqrt(n_sample / 20000.0)
+    radius = 20.0 * np.sqrt(n_sample / 1847.0)  # constant landmark density (synth.hpp:19-20)
     q0 = np.stack([radius * r * np.cos(golden * i), radius * r * np.sin(golden * i), radius * z], axis=1)
     p_true = (0.75 * oracle.rng_normals(0, n_sample * 3)).reshape(n_sample, 3)
     target = cpu.integrate_forward("f64", q0, p_true, SIGMA, timesteps)[0][-1]
@@ -205,9 +205,12 @@ def b200_arm(args):
     K, W = max(args.steps, 1), max(args.warmup, 3)
 
     # ---- workload (synthetic) ----
-    density_scaled = n > 20000  # keep point density when sweeping N upward
+    # Template radius grows with sqrt(N/1847) so the landmark density is that of the reference's default
+    # problem (synth.hpp:19-20: 1847 points on a 40 mm sphere).  At fixed 40 mm diameter N = 20 000 packs
+    # 4 landmarks/mm^2 against sigma = 1.5 mm and the flow turns chaotic (|target - q0| up to 1.2 m, loss
+    # 1e16, fp32 and fp64 differ by 0.6 %): not a meaningful evaluation point.  GPU time is data-independent.
     q0, target, _ = make_synthetic_pair(n, SIGMA, T, seed=0 if rows_mode else rank, device=local_rank,
-                                        density_scaled=density_scaled)
+                                        density_scaled=True)
     x0 = np.ascontiguousarray(((target - q0) / T).ravel())
 
     system = HamiltonianSystem(SIGMA, n, 3, prec, device=local_rank, max_timesteps=T, variant=args.variant)
@@ -280,6 +283,7 @@ def b200_arm(args):
                          f"single registration N={n}, T={T}, one fwd+bwd gradient per step"
                          + (f", {world} independent replicas" if distributed else "")),
             "n": n, "timesteps": T, "sigma": SIGMA, "lambda": LAMBDA, "units_per_step": "2*T*N^2",
+            "template": "Fibonacci sphere, radius 20*sqrt(N/1847) mm (constant landmark density)",
             "l2": "flushed between timed steps (256 MiB write)", "variant": args.variant,
             "kernel_variant": system.lib.lms_variant_name(0 if prec == "f32" else 1, args.variant).decode(),
         },

@@ -29,6 +29,8 @@ namespace lms {
 
 constexpr int kThreads = 128;  // threads per CTA
 constexpr int kTileJ = 128;    // columns staged per shared-memory tile
+constexpr int kUnitJ = 8;      // stream-K work unit: kUnitJ columns of one row tile
+constexpr int kUnitsPerTile = kTileJ / kUnitJ;
 
 enum Mode : int { kFwd = 0, kAdj = 1, kVel = 2 };
 
@@ -179,6 +181,99 @@ __device__ __forceinline__ void pair_term(const T* __restrict__ ri, const T* __r
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// fp32 packed path: sm_100a's two-wide FP32 instructions (FFMA2 / FADD2 / FMUL2).
+// A thread packs two of its rows into the halves of a 64-bit register pair; the column operand is
+// the same for both rows and enters as FFMA2's scalar-broadcast (.F32) operand.  Measured on B200 (profiles/ubench): FFMA2 sustains 128 lanes/SM/clk from HALF the issue
+// slots of scalar FFMA, and its 64-bit operand reads do not hit the register-bank dispatch stalls
+// that hold the scalar kernels at ~77 % issue utilisation (profiles/r1_ncu_v0_scalar.md).
+// Packed operands cannot take a free negation, so the terms are arranged with plus signs only:
+//   ndx = q_j - q_i (= -dx), nbv = b_i - b_j (= -db), nt = -inv_sig2 (ndx.nbv) (= -t)
+//   forward : acc[0..D) += (p_i.p_j) K ndx   (= -(p_i.p_j) K dx: negated once after the sweep)
+//   adjoint : acc[0..D) += K (pa - c t) ndx + K c nbv,   acc[D..2D) += K a_j + K nt p_j
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ float2 splat2(float v) { return make_float2(v, v); }
+
+__device__ __forceinline__ float2 ex2_pair(float2 x)
+{
+  float2 y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.x) : "f"(x.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.y) : "f"(x.y));
+  return y;
+}
+
+// ri2: packed row operands [nq (= -q_i), p, (alpha, beta)] or [nx]; cj2: duplicated column operands.
+template <int D, int MODE>
+__device__ __forceinline__ void pair_term_packed(const float2* __restrict__ ri2, const float2* __restrict__ cj2,
+                                                 float2* __restrict__ acc, float2 kexp2, float2 ns2, float2 neg1)
+{
+  float2 ndx[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) ndx[c] = __fadd2_rn(cj2[c], ri2[c]);
+  float2 r2 = __fmul2_rn(ndx[0], ndx[0]);
+#pragma unroll
+  for (int c = 1; c < D; ++c) r2 = __ffma2_rn(ndx[c], ndx[c], r2);
+  const float2 k = ex2_pair(__fmul2_rn(r2, kexp2));
+  if constexpr (MODE == kVel) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[c] = __ffma2_rn(k, cj2[D + c], acc[c]);
+  } else if constexpr (MODE == kFwd) {
+    float2 cc = __fmul2_rn(ri2[D], cj2[D]);
+#pragma unroll
+    for (int c = 1; c < D; ++c) cc = __ffma2_rn(ri2[D + c], cj2[D + c], cc);
+    const float2 s = __fmul2_rn(cc, k);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      acc[c] = __ffma2_rn(s, ndx[c], acc[c]);
+      acc[D + c] = __ffma2_rn(k, cj2[D + c], acc[D + c]);
+    }
+  } else {
+    const float2* pi = ri2 + D;
+    const float2* ai = ri2 + 2 * D;
+    const float2* bi = ri2 + 3 * D;
+    const float2* pj = cj2 + D;
+    const float2* aj = cj2 + 2 * D;
+    const float2* bj = cj2 + 3 * D;
+    float2 cc = __fmul2_rn(pi[0], pj[0]);
+    float2 pa = __fmul2_rn(pi[0], aj[0]);
+#pragma unroll
+    for (int c = 1; c < D; ++c) {
+      cc = __ffma2_rn(pi[c], pj[c], cc);
+      pa = __ffma2_rn(pi[c], aj[c], pa);
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) pa = __ffma2_rn(pj[c], ai[c], pa);
+    float2 nbv[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) nbv[c] = __ffma2_rn(bj[c], neg1, bi[c]);
+    float2 rb = __fmul2_rn(ndx[0], nbv[0]);
+#pragma unroll
+    for (int c = 1; c < D; ++c) rb = __ffma2_rn(ndx[c], nbv[c], rb);
+    const float2 nt = __fmul2_rn(rb, ns2);
+    const float2 w = __ffma2_rn(cc, nt, pa);
+    const float2 kw = __fmul2_rn(k, w);
+    const float2 kc = __fmul2_rn(k, cc);
+    const float2 knt = __fmul2_rn(k, nt);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      acc[c] = __ffma2_rn(kw, ndx[c], acc[c]);
+      acc[c] = __ffma2_rn(kc, nbv[c], acc[c]);
+      acc[D + c] = __ffma2_rn(k, aj[c], acc[D + c]);
+      acc[D + c] = __ffma2_rn(knt, pj[c], acc[D + c]);
+    }
+  }
+}
+
+// Row owned by (r, tid) in row tile rt.  Packed kernels pair rows (2*tid, 2*tid+1) of each 256-row group.
+template <int R, bool PACKED>
+__device__ __forceinline__ long long row_of(int rt, int r, int tid)
+{
+  if constexpr (PACKED)
+    return (long long)rt * (kThreads * R) + (r >> 1) * (2 * kThreads) + 2 * tid + (r & 1);
+  else
+    return (long long)rt * (kThreads * R) + r * kThreads + tid;
+}
+
 // Vector load of JU consecutive columns of one staged component.
 template <typename T, int JU>
 struct ColVec;
@@ -234,9 +329,10 @@ __device__ __forceinline__ double block_sum(double v, double* scratch)
 // ---------------------------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------------------------
-template <typename T, int D, int MODE, int R, int JU, int MINB>
+template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false>
 __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> a)
 {
+  static_assert(!PACKED || (sizeof(T) == 4 && R % 2 == 0), "the packed path is fp32 with an even row count");
   using S = Shape<MODE, D>;
   constexpr int NC = S::kColComps;
   constexpr int NR = S::kRowComps;
@@ -248,7 +344,9 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
   __shared__ int s_last;
 
   const int tid = threadIdx.x;
-  const long long nJ = a.n_j_tiles;
+  // Work is counted in units of kUnitJ columns of one row tile, so every CTA's share differs by at most
+  // one unit (1/16 of a staged tile); `cells` and `nJ` below are in those units.
+  const long long nJ = (long long)a.n_j_tiles * kUnitsPerTile;
   const long long cells = (long long)a.n_row_tiles * nJ;
   const long long G = gridDim.x;
   long long c = cells * blockIdx.x / G;
@@ -267,16 +365,19 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 
   while (c < c_end) {
     const long long rt_local = c / nJ;
-    const int jt0 = (int)(c - rt_local * nJ);
+    const int u0 = (int)(c - rt_local * nJ);  // unit range [u0, u1) of this row tile
     const long long span = c_end - c;
-    const int jt1 = (int)((long long)jt0 + span < nJ ? (long long)jt0 + span : nJ);
+    const int u1 = (int)((long long)u0 + span < nJ ? (long long)u0 + span : nJ);
+    const int col0 = u0 * kUnitJ, col1 = u1 * kUnitJ;  // column range, multiples of kUnitJ
+    const int jt0 = col0 / kTileJ;
+    const int jt1 = (col1 + kTileJ - 1) / kTileJ;
     const int rt = a.row_tile0 + (int)rt_local;
 
     // ---- row operands --------------------------------------------------------------------
     T ri[R][NR];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const long long row = (long long)rt * BM + r * kThreads + tid;
+      const long long row = row_of<R, PACKED>(rt, r, tid);
 #pragma unroll
       for (int k = 0; k < NR; ++k) {
         if constexpr (MODE == kAdj) {
@@ -294,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       for (int k = 0; k < NA; ++k) acc[r][k] = T(0);
 
     // ---- sweep the j tiles [jt0, jt1) with register-prefetched double buffering ---------------
+    // (only columns [col0, col1) of the first and last tile are accumulated)
     T stage[NC];
 #pragma unroll
     for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)jt0 * kTileJ + tid];
@@ -301,14 +403,38 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 #pragma unroll
     for (int k = 0; k < NC; ++k) tile[0][k][tid] = stage[k];
     __syncthreads();
+
+    // packed path only: two rows per 64-bit register pair; -q_i (or -x_i) first, the rest as they are
+    constexpr int RP = PACKED ? R / 2 : 1;
+    float2 ri2[RP][NR];
+    float2 acc2[RP][NA];
+    float2 kexp2, ns2, neg1;
+    if constexpr (PACKED) {
+#pragma unroll
+      for (int rp = 0; rp < RP; ++rp) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+          const float lo = (float)ri[2 * rp][k], hi = (float)ri[2 * rp + 1][k];
+          ri2[rp][k] = k < D ? make_float2(-lo, -hi) : make_float2(lo, hi);
+        }
+#pragma unroll
+        for (int k = 0; k < NA; ++k) acc2[rp][k] = make_float2(0.f, 0.f);
+      }
+      kexp2 = splat2((float)a.kexp);
+      ns2 = splat2(-(float)a.inv_sig2);
+      neg1 = splat2(-1.f);
+    }
+
     for (int jt = jt0; jt < jt1; ++jt) {
       const bool more = jt + 1 < jt1;
       if (more) {
 #pragma unroll
         for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)(jt + 1) * kTileJ + tid];
       }
+      const int jj_lo = col0 > jt * kTileJ ? col0 - jt * kTileJ : 0;
+      const int jj_hi = col1 < (jt + 1) * kTileJ ? col1 - jt * kTileJ : kTileJ;
 #pragma unroll 1
-      for (int jj = 0; jj < kTileJ; jj += JU) {
+      for (int jj = jj_lo; jj < jj_hi; jj += JU) {
         T cj[JU][NC];
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
@@ -317,10 +443,23 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 #pragma unroll
           for (int u = 0; u < JU; ++u) cj[u][k] = v[u];
         }
+        if constexpr (!PACKED) {
 #pragma unroll
-        for (int u = 0; u < JU; ++u)
+          for (int u = 0; u < JU; ++u)
 #pragma unroll
-          for (int r = 0; r < R; ++r) pair_term<T, D, MODE>(ri[r], cj[u], acc[r], a.kexp, a.inv_sig2);
+            for (int r = 0; r < R; ++r) pair_term<T, D, MODE>(ri[r], cj[u], acc[r], a.kexp, a.inv_sig2);
+        } else {
+#pragma unroll
+          for (int u = 0; u < JU; ++u) {
+            // the column operand is the same for both packed rows: ptxas folds splat2() into FFMA2's
+            // scalar-broadcast (.F32) operand form, so no register or shared-memory duplication is needed
+            float2 cj2[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) cj2[k] = splat2((float)cj[u][k]);
+#pragma unroll
+            for (int rp = 0; rp < RP; ++rp) pair_term_packed<D, MODE>(ri2[rp], cj2, acc2[rp], kexp2, ns2, neg1);
+          }
+        }
       }
       if (more) {
 #pragma unroll
@@ -328,6 +467,24 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       }
       __syncthreads();
       buf ^= 1;
+    }
+    if constexpr (PACKED) {
+      // back to the scalar convention of pair_term: forward acc[0..D) holds +(p_i.p_j) K dx.  The scalar
+      // row operands are rebuilt from the packed ones so that only one copy stays live across the sweep.
+#pragma unroll
+      for (int rp = 0; rp < RP; ++rp) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+          ri[2 * rp][k] = (T)(k < D ? -ri2[rp][k].x : ri2[rp][k].x);
+          ri[2 * rp + 1][k] = (T)(k < D ? -ri2[rp][k].y : ri2[rp][k].y);
+        }
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+          const bool flip = MODE == kFwd && k < D;
+          acc[2 * rp][k] = (T)(flip ? -acc2[rp][k].x : acc2[rp][k].x);
+          acc[2 * rp + 1][k] = (T)(flip ? -acc2[rp][k].y : acc2[rp][k].y);
+        }
+      }
     }
 
     // ---- combine partial sums across the CTAs that share this row tile ----------------------------
@@ -377,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       double hsum = 0.0, msum = 0.0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const long long row = (long long)rt * BM + r * kThreads + tid;
+        const long long row = row_of<R, PACKED>(rt, r, tid);
         const bool live = row < a.n_rows;
         if constexpr (MODE == kVel) {
           if (live) {
@@ -479,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         }
       }
     }
-    c += jt1 - jt0;
+    c += u1 - u0;
   }
 }
 

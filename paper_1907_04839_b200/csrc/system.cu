@@ -30,6 +30,7 @@ void dev_free(T*& p)
 // (R rows per thread, JU columns per shared-memory vector load, min CTAs/SM for __launch_bounds__).
 // Variant 0 is the default the library ships with; the rest are kept for on-GPU A/B (bench.py --variant).
 #define LMS_PICK(T, D, MODE, R, JU, MINB, NAME) make_choice<T, D, MODE, R, JU, MINB>(NAME)
+#define LMS_PICK2(D, MODE, R, JU, MINB, NAME) make_choice<float, D, MODE, R, JU, MINB, true>(NAME)
 
 template <>
 KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
@@ -38,6 +39,10 @@ KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
     case 1: return LMS_PICK(float, 3, kFwd, 2, 4, 4, "fwd_f32_r2_j4");
     case 2: return LMS_PICK(float, 3, kFwd, 4, 2, 3, "fwd_f32_r4_j2");
     case 3: return LMS_PICK(float, 3, kFwd, 2, 2, 6, "fwd_f32_r2_j2");
+    case 4: return LMS_PICK2(3, kFwd, 4, 2, 4, "fwd_f32x2_r4_j2");
+    case 5: return LMS_PICK2(3, kFwd, 2, 2, 6, "fwd_f32x2_r2_j2");
+    case 6: return LMS_PICK2(3, kFwd, 4, 1, 4, "fwd_f32x2_r4_j1");
+    case 7: return LMS_PICK2(3, kFwd, 6, 1, 3, "fwd_f32x2_r6_j1");
     default: return LMS_PICK(float, 3, kFwd, 4, 4, 3, "fwd_f32_r4_j4");
   }
 }
@@ -48,12 +53,17 @@ KernelChoice<float> pick_kernel<float, 3, kAdj>(int v)
     case 1: return LMS_PICK(float, 3, kAdj, 2, 4, 3, "adj_f32_r2_j4");
     case 2: return LMS_PICK(float, 3, kAdj, 4, 2, 2, "adj_f32_r4_j2");
     case 3: return LMS_PICK(float, 3, kAdj, 1, 4, 6, "adj_f32_r1_j4");
+    case 4: return LMS_PICK2(3, kAdj, 2, 2, 4, "adj_f32x2_r2_j2");
+    case 5: return LMS_PICK2(3, kAdj, 2, 1, 5, "adj_f32x2_r2_j1");
+    case 6: return LMS_PICK2(3, kAdj, 4, 1, 3, "adj_f32x2_r4_j1");
+    case 7: return LMS_PICK2(3, kAdj, 4, 2, 2, "adj_f32x2_r4_j2");
     default: return LMS_PICK(float, 3, kAdj, 2, 2, 4, "adj_f32_r2_j2");
   }
 }
 template <>
-KernelChoice<float> pick_kernel<float, 3, kVel>(int)
+KernelChoice<float> pick_kernel<float, 3, kVel>(int v)
 {
+  if (v >= 4) return LMS_PICK2(3, kVel, 4, 2, 4, "vel_f32x2_r4_j2");
   return LMS_PICK(float, 3, kVel, 4, 4, 4, "vel_f32_r4_j4");
 }
 template <>
@@ -224,15 +234,17 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   p.n_row_tiles = row_tiles >= 0 ? row_tiles : ceil_div(n_rows, p.bm);
   p.n_j_tiles = ceil_div((long long)cfg.n, kTileJ);
   (void)row_tile0;
-  const long long cells = (long long)p.n_row_tiles * p.n_j_tiles;
+  const long long units_per_row = (long long)p.n_j_tiles * kUnitsPerTile;  // work units, see pair_kernel
+  const long long cells = (long long)p.n_row_tiles * units_per_row;
   if (cells <= 0) return p;
   int per_sm = 0;
   LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kThreads, 0));
   per_sm = std::max(per_sm, 1);
   const long long full = (long long)num_sms_ * per_sm;
-  p.grid = (int)std::min<long long>(full, cells);
+  // never more CTAs than staged tiles: a CTA should sweep at least one full tile's worth of columns
+  p.grid = (int)std::min<long long>(full, std::max<long long>(cells / kUnitsPerTile, 1));
   const long long per_cta = (cells + p.grid - 1) / p.grid;
-  p.max_seg = (int)((per_cta + p.n_j_tiles - 1) / p.n_j_tiles) + 1;
+  p.max_seg = (int)((per_cta + units_per_row - 1) / units_per_row) + 1;
   constexpr int NA = Shape<MODE, D>::kAcc;
   p.partial_elems = (size_t)p.grid * p.max_seg * NA * p.bm;
   return p;
@@ -386,7 +398,8 @@ void System<T, D>::hamiltonian(const double* q, const double* p, double* out)
   a.out = scratch_out_;
   a.epi = kEpiRaw | kEpiFirstStep;
   launch<kFwd>(k_fwd_, a, plan);
-  finalize_scalars<0><<<1, 32, 0, stream_>>>(h_part_, mm_part_, plan.n_row_tiles, 0.0, d_scalars_);
+  // partials are indexed in 128-row units (rt * R), zero where no tile starts
+  finalize_scalars<0><<<1, 32, 0, stream_>>>(h_part_, mm_part_, part_tiles_, 0.0, d_scalars_);
   LMS_CUDA(cudaGetLastError());
   LMS_CUDA(cudaMemcpyAsync(h_scalars_, d_scalars_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   sync();

@@ -79,11 +79,11 @@ struct KernelChoice {
   const char* name = "";
 };
 
-template <typename T, int D, int MODE, int R, int JU, int MINB>
+template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false>
 KernelChoice<T> make_choice(const char* name)
 {
   KernelChoice<T> c;
-  c.fn = pair_kernel<T, D, MODE, R, JU, MINB>;
+  c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED>;
   c.rows_per_thread = R;
   c.name = name;
   return c;

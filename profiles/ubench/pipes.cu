@@ -131,6 +131,94 @@ __global__ void __launch_bounds__(256) pipe_kernel(float* out, long long* cycles
     }
 #pragma unroll
     for (int k = 0; k < 16; ++k) r += acc[k];
+  } else if constexpr (MODE == 9) {  // FFMA, three DISTINCT register sources per instruction, no operand reuse
+    float acc[16], x[16], y[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { acc[k] = threadIdx.x * 1e-3f + k; x[k] = a + k * 1e-3f * threadIdx.x; y[k] = b - k * 1e-3f * threadIdx.x; }
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc[k] = fmaf(x[k], y[k], acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) r += acc[k];
+  } else if constexpr (MODE == 10) {  // FFMA2, three distinct 64-bit register sources per instruction
+    float2 acc[8], x[8], y[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      acc[k] = make_float2(threadIdx.x * 1e-3f + k, k);
+      x[k] = make_float2(a + k * 1e-3f * threadIdx.x, a - k * 1e-3f * threadIdx.x);
+      y[k] = make_float2(b - k * 1e-3f * threadIdx.x, b + k * 1e-3f * threadIdx.x);
+    }
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = __ffma2_rn(x[k], y[k], acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r += acc[k].x + acc[k].y;
+  } else if constexpr (MODE == 11) {  // FFMA2, two distinct register sources + one reused
+    float2 acc[8], x[8];
+    float2 c2 = make_float2(a, b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      acc[k] = make_float2(threadIdx.x * 1e-3f + k, k);
+      x[k] = make_float2(a + k * 1e-3f * threadIdx.x, a - k * 1e-3f * threadIdx.x);
+    }
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = __ffma2_rn(x[k], c2, acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r += acc[k].x + acc[k].y;
+  } else if constexpr (MODE == 12) {  // FFMA, two distinct register sources + one reused
+    float acc[16], x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { acc[k] = threadIdx.x * 1e-3f + k; x[k] = a + k * 1e-3f * threadIdx.x; }
+    float c1 = b * threadIdx.x;
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc[k] = fmaf(x[k], c1, acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) r += acc[k];
+  } else if constexpr (MODE == 15) {  // FFMA2 acc2 += x2[k] * splat(y[k]): the .F32 broadcast operand form
+    float2 acc[8], x[8];
+    float y[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      acc[k] = make_float2(threadIdx.x * 1e-3f + k, k);
+      x[k] = make_float2(a + k * 1e-3f * threadIdx.x, a - k * 1e-3f * threadIdx.x);
+      y[k] = b - k * 1e-3f * threadIdx.x;
+    }
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = __ffma2_rn(x[k], make_float2(y[k], y[k]), acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r += acc[k].x + acc[k].y;
+  } else if constexpr (MODE == 13) {  // FMUL2 then dependent FFMA2 chain of length 3 x 8 independent (latency probe)
+    float2 acc[2], x[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) { acc[k] = make_float2(threadIdx.x * 1e-3f + k, k); x[k] = make_float2(a + k, a - k); }
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+      for (int rep = 0; rep < 4; ++rep)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) acc[k] = __ffma2_rn(acc[k], x[k], x[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) r += acc[k].x + acc[k].y;
+  } else if constexpr (MODE == 14) {  // scalar FFMA dependent chains, 2 independent (latency probe)
+    float acc[2], x[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) { acc[k] = threadIdx.x * 1e-3f + k; x[k] = a + k; }
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+      for (int rep = 0; rep < 8; ++rep)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) acc[k] = fmaf(acc[k], x[k], x[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) r += acc[k];
   }
   long long t1 = clock64();
   if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
@@ -178,6 +266,7 @@ int main(int argc, char** argv)
   std::vector<Result> results;
   std::vector<long long> h_cyc(grid);
 
+  int cur_grid = grid;
   auto run = [&](const char* name, auto launch, double winst_per_thread_iter, double lanes_per_winst) {
     for (int w = 0; w < 3; ++w) launch();
     CK(cudaDeviceSynchronize());
@@ -188,9 +277,9 @@ int main(int argc, char** argv)
     }
     CK(cudaMemcpy(h_cyc.data(), d_cyc, sizeof(long long) * grid, cudaMemcpyDeviceToHost));
     // all CTAs are co-resident, so the kernel's cycle span ~ max CTA cycles
-    long long cmax = 0; for (auto c : h_cyc) cmax = c > cmax ? c : cmax;
+    long long cmax = 0; for (int i = 0; i < cur_grid; ++i) cmax = h_cyc[i] > cmax ? h_cyc[i] : cmax;
     double mhz = cmax / (best * 1e-3) / 1e6;
-    double warps_per_sm = ctas_per_sm * 8.0;
+    double warps_per_sm = (double)cur_grid / sms * 8.0;
     double winst = warps_per_sm * ITER * winst_per_thread_iter;  // per SM
     double per_clk = winst / cmax;
     results.push_back({name, best, mhz, per_clk, per_clk * 32 * lanes_per_winst});
@@ -198,6 +287,20 @@ int main(int argc, char** argv)
            per_clk, per_clk * 32 * lanes_per_winst);
   };
 
+#define RUNK(NAME, KERN, PTR, A, B, W, L)                                                        \
+  {                                                                                               \
+    int per_sm = 0;                                                                               \
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, KERN, 256, 0));                     \
+    if (per_sm > ctas_per_sm) per_sm = ctas_per_sm;                                               \
+    cur_grid = sms * per_sm;                                                                      \
+    run(NAME, [&] { KERN<<<cur_grid, 256>>>(PTR, d_cyc, A, B); }, W, L);                          \
+  }
+  RUNK("ffma_3reg_distinct", pipe_kernel<9>, d_out, 1.0001f, 0.5f, 16, 1)
+  RUNK("ffma2_3reg_distinct", pipe_kernel<10>, d_out, 1.0001f, 0.5f, 8, 2)
+  RUNK("ffma2_2reg_1reused", pipe_kernel<11>, d_out, 1.0001f, 0.5f, 8, 2)
+  RUNK("ffma_2reg_1reused", pipe_kernel<12>, d_out, 1.0001f, 0.5f, 16, 1)
+  RUNK("ffma2_f32_broadcast_operand", pipe_kernel<15>, d_out, 1.0001f, 0.5f, 8, 2)
+  cur_grid = grid;
   run("ffma", [&] { pipe_kernel<0><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 16, 1);
   run("ffma2_packed", [&] { pipe_kernel<1><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 8, 2);
   run("fadd", [&] { pipe_kernel<2><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 16, 1);
@@ -207,6 +310,8 @@ int main(int argc, char** argv)
   run("mix_8ffma2_2mufu", [&] { pipe_kernel<6><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 10, 1.8);
   run("fadd2_packed", [&] { pipe_kernel<7><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 8, 2);
   run("ffma_3src", [&] { pipe_kernel<8><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 20, 1);
+  run("ffma2_dep_chain_ilp2", [&] { pipe_kernel<13><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 8, 2);
+  run("ffma_dep_chain_ilp2", [&] { pipe_kernel<14><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 16, 1);
   run("dfma", [&] { pipe_kernel_f64<0><<<grid, 256>>>(d_out64, d_cyc, 1.0001, 0.5); }, 8, 1);
   run("dadd", [&] { pipe_kernel_f64<1><<<grid, 256>>>(d_out64, d_cyc, 1.0001, 0.5); }, 8, 1);
   run("dmul", [&] { pipe_kernel_f64<2><<<grid, 256>>>(d_out64, d_cyc, 1.0001, 0.5); }, 8, 1);
