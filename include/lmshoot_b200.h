@@ -177,6 +177,10 @@ int lms_register(lms_system* sys, const lms_lbfgs_params* params, double* moment
  * state after every time step over NCCL.  unique_id is the 128-byte ncclUniqueId produced by
  * lms_comm_unique_id() on rank 0 and broadcast by the caller. */
 int lms_comm_unique_id(unsigned char id[128]);
+/* The partition itself (host arithmetic, no device needed): every rank owns `slice` rows of a plane padded
+ * to `stride` = slice * world; the live rows of `rank` are [row_begin, row_end). */
+int lms_row_partition(size_t n, int world, int rank, long long* slice, long long* stride, long long* row_begin,
+                      long long* row_end);
 int lms_system_comm_init(lms_system* sys, const unsigned char id[128], int rank, int world);
 
 /* ---- synthetic inputs (synth.hpp:15-43, rng.hpp) ---- */

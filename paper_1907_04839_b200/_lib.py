@@ -90,6 +90,8 @@ SIGNATURES = {
     ),
     "lms_register": ([c_void_p, POINTER(LmsLbfgsParams), _dp, _dp, POINTER(LmsMinimizeResult), _dp], c_int),
     "lms_comm_unique_id": ([POINTER(c_ubyte)], c_int),
+    "lms_row_partition": ([c_size_t, c_int, c_int, POINTER(c_longlong), POINTER(c_longlong), POINTER(c_longlong),
+                           POINTER(c_longlong)], c_int),
     "lms_system_comm_init": ([c_void_p, POINTER(c_ubyte), c_int, c_int], c_int),
     "lms_rng_normals": ([c_uint64, c_size_t, _dp], None),
     "lms_rng_uniforms": ([c_uint64, c_size_t, _dp], None),

@@ -221,6 +221,18 @@ int lms_comm_unique_id(unsigned char id[128])
   return LMS_OK;
 }
 
+int lms_row_partition(size_t n, int world, int rank, long long* slice, long long* stride, long long* row_begin,
+                      long long* row_end)
+{
+  if (world < 1 || rank < 0 || rank >= world) return LMS_ERR_INVALID;
+  const lms::RowPartition p = lms::partition_rows((long long)n, world, rank);
+  if (slice) *slice = p.slice;
+  if (stride) *stride = p.stride;
+  if (row_begin) *row_begin = p.row_begin;
+  if (row_end) *row_end = p.row_end;
+  return LMS_OK;
+}
+
 int lms_system_comm_init(lms_system* sys, const unsigned char id[128], int rank, int world)
 {
   return guarded(sys, [&](lms::SystemBase* s) { s->comm_init(id, rank, world); });

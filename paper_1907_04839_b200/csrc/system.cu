@@ -1,6 +1,8 @@
 // System<T,D>: implementation.  See system.cuh.
 #include "system.cuh"
 
+#include <cstdlib>
+
 namespace lms {
 
 namespace {
@@ -445,7 +447,7 @@ void System<T, D>::integrate_forward(const double* q0, const double* p0, int tim
 {
   if (timesteps < 1) throw StatusError{LMS_ERR_INVALID, "timesteps must be >= 1"};
   if (timesteps > max_t_) throw StatusError{LMS_ERR_INVALID, "timesteps exceeds cfg.max_timesteps"};
-  if (world_ > 1) throw StatusError{LMS_ERR_STATE, "integrate_forward is single-GPU; use the bound objective"};
+  if (comm_active_) throw StatusError{LMS_ERR_STATE, "integrate_forward is single-GPU; use the bound objective"};
   stored_t_ = -1;
   traj0_is_q0_ = false;
   if (n() == 0) {
@@ -514,7 +516,7 @@ void System<T, D>::bind(const double* q0, const double* target, double lambda_in
     ensure_partials(std::max(plan_fwd_.partial_elems, plan_adj_.partial_elems),
                     std::max(plan_fwd_.n_row_tiles, plan_adj_.n_row_tiles));
     sync();
-    if (world_ == 1) {
+    if (!comm_active_) {
       // Capture the whole evaluation (2T+2 kernels) into one CUDA graph: at small N the 2T dependent
       // launches are pure latency (SURVEY.md §7 "Small-N latency").
       cudaGraph_t g = nullptr;
@@ -571,12 +573,12 @@ void System<T, D>::enqueue_eval(bool timed)
     if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
     launch<kFwd>(k_fwd_, a, plan_fwd_);
     if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
-    if (world_ > 1) {
+    if (comm_active_) {
       all_gather_state(snapshot(t + 1));
       if (t == Tn - 1) all_gather_state(adj_[0]);
     }
   }
-  if (world_ > 1) {
+  if (comm_active_) {
     all_gather_doubles(h_part_);
     all_gather_doubles(mm_part_);
   }
@@ -596,10 +598,10 @@ void System<T, D>::enqueue_eval(bool timed)
     if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
     launch<kAdj>(k_adj_, a, plan_adj_);
     if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
-    if (world_ > 1 && t > 0) all_gather_state(adj_[cur ^ 1]);
+    if (comm_active_ && t > 0) all_gather_state(adj_[cur ^ 1]);
     cur ^= 1;
   }
-  if (world_ > 1) {
+  if (comm_active_) {
     // every rank ends with the full gradient (row-major double rows are contiguous per rank slice)
     const NcclApi& nc = nccl_api();
     const size_t slice = (size_t)(stride_ / world_) * D;
@@ -754,16 +756,17 @@ template <typename T, int D>
 void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
 {
   if (world < 1 || rank < 0 || rank >= world) throw StatusError{LMS_ERR_INVALID, "bad rank/world"};
-  if (world == 1) return;
+  // world == 1 normally needs no communicator; LMS_FORCE_NCCL=1 keeps the NCCL path on so that a single-GPU
+  // box can exercise it (tests/test_gpu_parity.py::test_nccl_path_single_rank).
+  const char* force = std::getenv("LMS_FORCE_NCCL");
+  if (world == 1 && !(force && force[0] == '1')) return;
   const NcclApi& nc = nccl_api();
   if (!nc.ok) throw StatusError{LMS_ERR_COMM, "libnccl.so.2 could not be loaded"};
   sync();
   destroy_graph();
   bound = false;
   // Re-lay the planes so that every rank owns an equal, tile-aligned slice (in-place all-gather).
-  const long long N = (long long)cfg.n;
-  const long long slice = std::max<long long>(round_up((N + world - 1) / world, kRowAlign), kRowAlign);
-  const long long new_stride = slice * world;
+  const long long new_stride = partition_rows((long long)cfg.n, world, rank).stride;
   if (new_stride != stride_) {
     stride_ = new_stride;
     const size_t plane = (size_t)stride_;
@@ -789,6 +792,7 @@ void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
   if (nc.CommInitRank(&comm_, world, uid, rank) != 0) throw StatusError{LMS_ERR_COMM, "ncclCommInitRank failed"};
   rank_ = rank;
   world_ = world;
+  comm_active_ = true;
 }
 
 // In-place all-gather of every plane of a (q,p) or (alpha,beta) state: rank r contributes rows
@@ -816,6 +820,18 @@ void System<T, D>::all_gather_doubles(double* buf)
   const size_t slice = (size_t)(part_tiles_ / world_);
   if (nc.AllGather(buf + rank_ * slice, buf, slice, kNcclFloat64, comm_, stream_) != 0)
     throw StatusError{LMS_ERR_COMM, "ncclAllGather(partials) failed"};
+}
+
+RowPartition partition_rows(long long n, int world, int rank)
+{
+  // Equal, tile-aligned slices so the per-step exchange is one in-place all-gather per plane: the chunk
+  // formula of parallel.cpp:145-146 applied to kRowAlign-row blocks, every rank padded to the same count.
+  RowPartition p;
+  p.slice = std::max<long long>(round_up((n + world - 1) / world, kRowAlign), kRowAlign);
+  p.stride = p.slice * world;
+  p.row_begin = std::min<long long>(p.slice * rank, n);
+  p.row_end = std::min<long long>(p.slice * (rank + 1), n);
+  return p;
 }
 
 const char* variant_name(int precision, int variant)

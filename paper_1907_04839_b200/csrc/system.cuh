@@ -192,10 +192,19 @@ class System final : public SystemBase {
 
   // row partition (multi-GPU)
   int rank_ = 0, world_ = 1;
+  bool comm_active_ = false;
   ncclComm_t comm_ = nullptr;
   int row_tile_begin_(int bm) const;
   int row_tile_end_(int bm) const;
 };
+
+struct RowPartition {
+  long long slice = 0;      // rows per rank (multiple of kRowAlign), identical on every rank
+  long long stride = 0;     // padded plane length = slice * world
+  long long row_begin = 0;  // live rows owned by this rank: [row_begin, row_end)
+  long long row_end = 0;
+};
+RowPartition partition_rows(long long n, int world, int rank);
 
 SystemBase* create_system(const lms_config& cfg);
 const char* variant_name(int precision, int variant);

@@ -261,3 +261,14 @@ def comm_unique_id() -> bytes:
     buf = (ctypes.c_ubyte * 128)()
     _lib.check(lib.lms_comm_unique_id(buf))
     return bytes(buf)
+
+
+def row_partition(n, world, rank):
+    """The row partition of the multi-GPU path (lms_row_partition): returns (slice, stride, row_begin, row_end).
+    Host arithmetic only; usable without a device."""
+    from ctypes import c_longlong
+
+    lib = _lib.load()
+    vals = [c_longlong() for _ in range(4)]
+    _lib.check(lib.lms_row_partition(n, world, rank, *[ctypes.byref(v) for v in vals]))
+    return tuple(v.value for v in vals)

@@ -394,3 +394,76 @@ def test_hundred_iteration_registration_n1000(oracle, reference):
     cfg32 = ShootingConfig(sigma=SIGMA, timesteps=T, lam=lam, max_iter=100, precision="f32")
     got32 = register_landmarks(q0, target, cfg32)
     assert np.abs(got32.warped - want["warped"]).max() <= 5e-3
+
+
+def test_reference_minimize_drives_cuda_objective_through_cpp_adapter():
+    """Drop-in check: the reference's UNMODIFIED minimize (lbfgs.cpp compiled in place into
+    oracle/_ref/libref_cuda_driver.so) calls the CUDA objective through include/lmshoot_b200/objective.hpp.
+    Same deterministic objective, two drivers (the reference's and the library's own): identical iterates."""
+    import ctypes
+    import os
+
+    from paper_1907_04839_b200 import ShootingConfig, register_landmarks
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                        "libref_cuda_driver.so")
+    if not os.path.exists(path):
+        pytest.skip("oracle/_ref/libref_cuda_driver.so not built (needs /root/reference at build time)")
+    lib = ctypes.CDLL(path)
+
+    class Out(ctypes.Structure):
+        _fields_ = [("loss", ctypes.c_double), ("initial_loss", ctypes.c_double), ("evaluations", ctypes.c_int),
+                    ("iterations", ctypes.c_int), ("reason", ctypes.c_int), ("status", ctypes.c_int),
+                    ("diverged_step", ctypes.c_int)]
+
+    dp = ctypes.POINTER(ctypes.c_double)
+    lib.ref_cuda_register.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_size_t, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_int, ctypes.c_int, ctypes.c_double, dp, dp, dp, dp,
+                                      ctypes.POINTER(Out), dp]
+    n, T, lam, iters = 700, 8, 1e4, 25
+    rng = np.random.default_rng(12)
+    q0 = rng.uniform(-12, 12, (n, 3))
+    target = q0 + 0.5 * rng.normal(size=(n, 3))
+    for prec in ("f64", "f32"):
+        mom, warped, hist = np.empty((n, 3)), np.empty((n, 3)), np.zeros(iters)
+        out = Out()
+        rc = lib.ref_cuda_register(int(prec == "f32"), 3, n, SIGMA, lam, T, iters, 1e-6, q0.ctypes.data_as(dp),
+                                   target.ctypes.data_as(dp), mom.ctypes.data_as(dp), warped.ctypes.data_as(dp),
+                                   ctypes.byref(out), hist.ctypes.data_as(dp))
+        assert rc == 0
+        mine = register_landmarks(q0, target, ShootingConfig(sigma=SIGMA, timesteps=T, lam=lam, max_iter=iters,
+                                                             precision=prec))
+        assert (out.evaluations, out.iterations) == (mine.evaluations, mine.iterations)
+        assert out.loss == mine.final_loss and out.initial_loss == mine.initial_loss
+        assert np.array_equal(mom, mine.momenta) and np.array_equal(warped, mine.warped)
+        assert np.array_equal(hist[: out.iterations], mine.hist_loss)
+        assert mine.final_loss < 0.05 * mine.initial_loss
+    # the adapter rethrows the reference's DivergedError with its timestep
+    bad = q0.copy()
+    bad[0, 0] = np.inf
+    out = Out()
+    rc = lib.ref_cuda_register(0, 3, n, SIGMA, lam, T, 3, 1e-6, bad.ctypes.data_as(dp), target.ctypes.data_as(dp),
+                               mom.ctypes.data_as(dp), warped.ctypes.data_as(dp), ctypes.byref(out),
+                               hist.ctypes.data_as(dp))
+    assert rc == 2 and out.diverged_step == 0
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_nccl_path_single_rank(hs, monkeypatch, prec):
+    """The row-partitioned code path (NCCL communicator, per-step in-place all-gathers, no CUDA graph) with a
+    world of one rank on the single GPU: must give the same bits as the plain path."""
+    from paper_1907_04839_b200 import HamiltonianSystem, comm_unique_id
+
+    n, T = 1500, 6
+    q, p, target, *_ = synth_case(n, 3, 77, spread=9.0)
+    plain = hs(n, 3, prec)
+    plain.bind_registration(q, target, 100.0, T)
+    want = plain.objective(p)
+    monkeypatch.setenv("LMS_FORCE_NCCL", "1")
+    s = HamiltonianSystem(SIGMA, n, 3, prec, max_timesteps=T)
+    s.comm_init(comm_unique_id(), 0, 1)
+    s.bind_registration(q, target, 100.0, T)
+    got = s.objective(p)
+    assert got[0] == want[0] and np.array_equal(got[1], want[1])
+    assert np.array_equal(s.final_q(), plain.final_q())
+    s.close()
