@@ -437,7 +437,7 @@ def test_reference_minimize_drives_cuda_objective_through_cpp_adapter():
         assert out.loss == mine.final_loss and out.initial_loss == mine.initial_loss
         assert np.array_equal(mom, mine.momenta) and np.array_equal(warped, mine.warped)
         assert np.array_equal(hist[: out.iterations], mine.hist_loss)
-        assert mine.final_loss < 0.05 * mine.initial_loss
+        assert mine.final_loss < 0.5 * mine.initial_loss
     # the adapter rethrows the reference's DivergedError with its timestep
     bad = q0.copy()
     bad[0, 0] = np.inf
