@@ -43,6 +43,7 @@ def parse_args():
     ap.add_argument("--timesteps", type=int, default=0)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--mode", default="rows", choices=["rows", "replicas"])
+    ap.add_argument("--batch", type=int, default=0, help="population mode: B registrations of --n landmarks per GPU")
     ap.add_argument("--no-extras", action="store_true", help="skip fp64, L-BFGS and cpu_baseline legs")
     ap.add_argument("--lbfgs-iters", type=int, default=5)
     return ap.parse_args()
@@ -385,10 +386,80 @@ def b200_arm(args):
         dist.destroy_process_group()
 
 
+def batch_arm(args):
+    """BASELINE configs[3]: a population of independent registrations (default 128 x N=2000 per GPU, the per-GPU
+    share of 1024 problems on 8 GPUs), one batched objective evaluation per step.  No collective: weak scaling."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1907_04839_b200 import BatchedRegistrations, make_template_points, rng_normals, HamiltonianSystem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    B, n, T = args.batch, args.n or 2000, args.timesteps or 10
+    K, W = max(args.steps, 1), max(args.warmup, 3)
+    q0 = np.empty((B, n, 3))
+    target = np.empty((B, n, 3))
+    base = make_template_points(n, 40.0 * float(np.sqrt(n / 1847.0)))
+    gen = HamiltonianSystem(SIGMA, n, 3, "f64", device=local_rank, max_timesteps=T)
+    for b in range(B):  # seeds 0..1023 across the population (SURVEY.md §8d C4)
+        p_true = (0.75 * rng_normals(rank * B + b, n * 3)).reshape(n, 3)
+        q0[b] = base
+        target[b] = gen.integrate_forward(base, p_true, T)[0][-1]
+    gen.close()
+    x0 = (target - q0) / T
+    br = BatchedRegistrations(SIGMA, n, B, 3, args.precision, device=local_rank, max_timesteps=T, variant=args.variant)
+    br.bind(q0, target, LAMBDA, T)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(W):
+        br.evaluate(x0)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev_ms = wall_ms = 0.0
+    for _ in range(K):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        br.evaluate(x0)
+        wall_ms += (time.perf_counter() - t0) * 1e3
+        dev_ms += br.last_eval_device_ms()
+    if world > 1:
+        t = torch.tensor([dev_ms, wall_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, wall_ms = float(t[0]), float(t[1])
+    units = 2.0 * T * float(n) * float(n) * B * world
+    line = {
+        "metric": "pair_kernel_evals_per_sec_per_gradient", "value": units * K / (dev_ms * 1e-3),
+        "unit": "pair-evals/s", "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": dev_ms / K,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": f"population: {B} independent registrations of N={n}, T={T} per GPU, one batched "
+                               f"fwd+bwd gradient of all problems per step", "n": n, "batch_per_gpu": B, "timesteps": T,
+                   "sigma": SIGMA, "lambda": LAMBDA, "l2": "flushed between timed steps (256 MiB write)"},
+        "e2e": {"value": units * K / (wall_ms * 1e-3), "unit": "pair-evals/s", "h2d_bytes_per_step": int(x0.nbytes),
+                "d2h_bytes_per_step": int(x0.nbytes) + 32 * B, "ms_per_step": wall_ms / K},
+        "gpu_launches": (2 * T + 2) * K,
+        "registrations_per_sec_per_gradient": B * world * K / (dev_ms * 1e-3),
+    }
+    br.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         reference_arm(args)
+    elif args.batch > 0:
+        batch_arm(args)
     else:
         b200_arm(args)
 

@@ -170,6 +170,32 @@ int lms_minimize(lms_objective_fn fn, void* user, size_t n, const double* x0,
 int lms_register(lms_system* sys, const lms_lbfgs_params* params, double* momenta_out,
                  double* warped_out, lms_minimize_result* result, double* hist_loss);
 
+/* ---- population batches (BASELINE configs[3]; no counterpart in the single-problem reference) ---- */
+
+/* A handle that holds `batch` independent registrations of cfg->n landmarks each (same sigma, dim,
+ * precision, lambda, timesteps).  Every O(N^2) launch covers all requested problems at once, so many
+ * small problems fill the GPU.  Arrays are batch-major: problem b occupies [b*n*dim, (b+1)*n*dim).
+ * lms_bind_registration() on such a handle takes batch x n x dim templates and targets. */
+int lms_batch_create(const lms_config* cfg, size_t batch, lms_system** out);
+size_t lms_batch_size(const lms_system* sys);
+
+/* One objective evaluation (registration.cpp:58-74) for `count` problems listed in ids (all problems
+ * when ids == NULL).  x, grad: batch x n x dim; scalars: batch x 3 = {loss, kinetic, mismatch};
+ * diverged_step (may be NULL): batch entries, -1 = finite, else DivergedError's timestep.  Only the
+ * listed problems' entries are read and written. */
+int lms_batch_eval(lms_system* sys, size_t count, const int* ids, const double* x, double* grad, double* scalars,
+                   int* diverged_step);
+
+/* q(1) of every problem after the last evaluation: batch x n x dim. */
+int lms_batch_final_q(lms_system* sys, double* out);
+
+/* register_impl core (registration.cpp:43-93) for every problem of the batch: each problem runs its own
+ * minimize (lbfgs.hpp:81-82) on a host thread; concurrent objective calls are coalesced into one batched
+ * device evaluation per round.  momenta_out / warped_out: batch x n x dim; results / status: batch entries
+ * (status = LMS_OK, LMS_ERR_DIVERGED or LMS_ERR_NUMERICAL per problem). */
+int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* momenta_out, double* warped_out,
+                       lms_minimize_result* results, int* status, int* rounds_out);
+
 /* ---- multi-GPU row partition (no counterpart in the single-process reference) ---- */
 
 /* Rank `rank` of `world` owns the contiguous row block [n*rank/world, n*(rank+1)/world) rounded to

@@ -3,6 +3,7 @@
 
 Importing this package does not touch the GPU; the C-ABI library is loaded on first use and its
 absence is an error (no CPU fallback)."""
+from .batch import BatchedRegistrations, BatchRegistrationResult  # noqa: F401
 from .errors import CommError, CudaError, DivergedError, NumericalError, ShapeError, StateError  # noqa: F401
 from .lbfgs import LbfgsParams, MinimizeResult, minimize  # noqa: F401
 from .registration import RegistrationResult, register_landmarks  # noqa: F401
@@ -11,7 +12,7 @@ from .shooting import (GradientResult, HamiltonianSystem, ShootingConfig, comm_u
 from .synth import make_synthetic_pair, make_template_points, rng_normals, rng_uniforms  # noqa: F401
 
 __all__ = [
-    "HamiltonianSystem", "ShootingConfig", "GradientResult", "LbfgsParams", "MinimizeResult", "minimize",
+    "HamiltonianSystem", "BatchedRegistrations", "BatchRegistrationResult", "ShootingConfig", "GradientResult", "LbfgsParams", "MinimizeResult", "minimize",
     "register_landmarks", "RegistrationResult", "make_synthetic_pair", "make_template_points", "rng_normals",
     "rng_uniforms", "gaussian_kernel", "kernel_scale", "comm_unique_id", "row_partition", "ShapeError", "DivergedError",
     "NumericalError", "CudaError", "StateError", "CommError",

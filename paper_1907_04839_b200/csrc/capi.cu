@@ -1,9 +1,12 @@
 // extern "C" surface of liblmshoot_b200.so (include/lmshoot_b200.h).  Exceptions never cross it.
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <random>
+#include <thread>
 
 #include "system.cuh"
 
@@ -96,6 +99,50 @@ int lms_system_create(const lms_config* cfg, lms_system** out)
   }
   *out = h;
   return LMS_OK;
+}
+
+int lms_batch_create(const lms_config* cfg, size_t batch, lms_system** out)
+{
+  if (!cfg || !out || batch < 1 || batch > (size_t)1 << 20) return LMS_ERR_INVALID;
+  *out = nullptr;
+  if (cfg->dim != 2 && cfg->dim != 3) return LMS_ERR_SHAPE;
+  if (!(cfg->sigma > 0)) return LMS_ERR_INVALID;
+  if (cfg->precision != LMS_PRECISION_F32 && cfg->precision != LMS_PRECISION_F64) return LMS_ERR_INVALID;
+  if (cfg->max_timesteps < 1) return LMS_ERR_INVALID;
+  if (cfg->n * batch > (size_t)0x7fffffff - 1024) return LMS_ERR_INVALID;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || cfg->device < 0 || cfg->device >= count) {
+    cudaGetLastError();
+    return LMS_ERR_CUDA;
+  }
+  lms_system* h = new (std::nothrow) lms_system;
+  if (!h) return LMS_ERR_CUDA;
+  h->device = cfg->device;
+  try {
+    h->impl = lms::create_system(*cfg, (int)batch);
+  } catch (const lms::StatusError& e) {
+    delete h;
+    return e.code;
+  } catch (...) {
+    cudaGetLastError();
+    delete h;
+    return LMS_ERR_CUDA;
+  }
+  *out = h;
+  return LMS_OK;
+}
+
+size_t lms_batch_size(const lms_system* sys) { return sys && sys->impl ? (size_t)sys->impl->batch : 0; }
+
+int lms_batch_eval(lms_system* sys, size_t count, const int* ids, const double* x, double* grad, double* scalars,
+                   int* diverged_step)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->eval_batch(x, grad, scalars, diverged_step, (int)count, ids); });
+}
+
+int lms_batch_final_q(lms_system* sys, double* out)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->final_q_batch(out); });
 }
 
 void lms_system_destroy(lms_system* sys)
@@ -270,6 +317,123 @@ int lms_register(lms_system* sys, const lms_lbfgs_params* params, double* moment
   rc = lms_objective_eval(sys, momenta_out, g.data(), &loss, nullptr, nullptr);
   if (rc != LMS_OK) return rc;
   return lms_objective_final_q(sys, warped_out);
+}
+
+// ---- population batches: one minimize per problem, objective calls coalesced per round ----
+namespace {
+
+// Every optimiser thread submits its trial point and sleeps; the last submitter of a round launches one batched
+// evaluation for all waiting problems and wakes them.  The drivers stay unchanged blocking callbacks.
+struct Rendezvous {
+  lms_system* sys;
+  size_t per;  // n * dim
+  std::mutex m;
+  std::condition_variable cv;
+  int active = 0, submitted = 0, rounds = 0;
+  unsigned long long round = 0;
+  std::vector<int> waiting;  // problem ids submitted this round
+  std::vector<double> x, grad, scalars;
+  std::vector<int> diverged;
+  int failure = LMS_OK;  // a CUDA-level failure aborts everybody
+
+  void run_round()  // caller holds the lock; everyone else is asleep
+  {
+    int rc = lms_batch_eval(sys, waiting.size(), waiting.data(), x.data(), grad.data(), scalars.data(),
+                            diverged.data());
+    if (rc != LMS_OK) failure = rc;
+    waiting.clear();
+    submitted = 0;
+    ++round;
+    ++rounds;
+    cv.notify_all();
+  }
+};
+
+struct ProblemCtx {
+  Rendezvous* rv;
+  int id;
+  int diverged_step = -1;
+};
+
+double batched_objective(void* user, const double* x, double* grad, size_t n)
+{
+  ProblemCtx* ctx = static_cast<ProblemCtx*>(user);
+  Rendezvous& rv = *ctx->rv;
+  std::unique_lock<std::mutex> lock(rv.m);
+  std::memcpy(rv.x.data() + ctx->id * rv.per, x, n * sizeof(double));
+  rv.waiting.push_back(ctx->id);
+  ++rv.submitted;
+  const unsigned long long my_round = rv.round;
+  if (rv.submitted == rv.active)
+    rv.run_round();
+  else
+    rv.cv.wait(lock, [&] { return rv.round != my_round; });
+  if (rv.failure != LMS_OK) throw rv.failure;
+  if (rv.diverged[ctx->id] >= 0) {
+    ctx->diverged_step = rv.diverged[ctx->id];
+    throw (int)LMS_ERR_DIVERGED;  // aborts this problem's minimize, as DivergedError does in the reference
+  }
+  std::memcpy(grad, rv.grad.data() + ctx->id * rv.per, n * sizeof(double));
+  return rv.scalars[3 * ctx->id];
+}
+
+}  // namespace
+
+int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* momenta_out, double* warped_out,
+                       lms_minimize_result* results, int* status, int* rounds_out)
+{
+  if (!sys || !sys->impl || !params || !momenta_out || !results || !status) return LMS_ERR_INVALID;
+  lms::SystemBase* s = sys->impl;
+  if (!s->bound) return LMS_ERR_STATE;
+  const int B = s->batch;
+  const size_t per = s->host_q0.size() / (size_t)B;
+  Rendezvous rv;
+  rv.sys = sys;
+  rv.per = per;
+  rv.active = B;
+  rv.x.assign(per * B, 0.0);
+  rv.grad.assign(per * B, 0.0);
+  rv.scalars.assign(3 * (size_t)B, 0.0);
+  rv.diverged.assign(B, -1);
+  std::vector<ProblemCtx> ctx(B);
+  std::vector<std::thread> threads;
+  threads.reserve(B);
+  for (int b = 0; b < B; ++b) {
+    ctx[b].rv = &rv;
+    ctx[b].id = b;
+    threads.emplace_back([&, b] {
+      std::vector<double> x0(per), g(per);
+      for (size_t e = 0; e < per; ++e)  // x0 = (target - q0)/T, registration.cpp:47-52
+        x0[e] = (s->host_target[b * per + e] - s->host_q0[b * per + e]) / s->timesteps;
+      int rc;
+      try {
+        rc = lms_minimize(batched_objective, &ctx[b], per, x0.data(), params, momenta_out + b * per, g.data(),
+                          &results[b], nullptr, nullptr, nullptr, nullptr);
+      } catch (int code) {
+        rc = code;
+      }
+      status[b] = rc;
+      std::unique_lock<std::mutex> lock(rv.m);
+      --rv.active;  // this problem no longer takes part in rounds
+      if (rv.active > 0 && rv.submitted == rv.active) rv.run_round();
+    });
+  }
+  for (auto& t : threads) t.join();
+  if (rounds_out) *rounds_out = rv.rounds;
+  if (rv.failure != LMS_OK) return rv.failure;
+  if (warped_out) {
+    // final re-integration under every p0* (registration.cpp:85-93): one more batched evaluation
+    std::vector<int> ok;
+    for (int b = 0; b < B; ++b)
+      if (status[b] == LMS_OK) ok.push_back(b);
+    if (!ok.empty()) {
+      int rc = lms_batch_eval(sys, ok.size(), ok.data(), momenta_out, rv.grad.data(), rv.scalars.data(),
+                              rv.diverged.data());
+      if (rc != LMS_OK) return rc;
+    }
+    return lms_batch_final_q(sys, warped_out);
+  }
+  return LMS_OK;
 }
 
 // ---- synthetic inputs ----

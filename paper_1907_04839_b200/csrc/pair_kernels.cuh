@@ -80,6 +80,12 @@ struct PairArgs {
   T two_lambda;
   unsigned epi;
   int step;  // time step whose state this launch produces (for the divergence record)
+  // batch of independent problems (population studies): row tile t of this launch belongs to problem
+  // batch_ids[t / tiles_per_problem] (identity when null); every pointer above is problem 0's and the
+  // strides below (in elements of the pointed-to type) step to the next problem.  Single problem: all zero.
+  int tiles_per_problem;
+  const int* batch_ids;
+  long long bs_j, bs_adj, bs_out, bs_seed, bs_vec, bs_grad, bs_part, bs_div;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -353,16 +359,6 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
   const long long c_end = cells * (blockIdx.x + 1) / G;
   const long long first_rt_local = c / nJ;  // first row tile (local index) this CTA touches
 
-  // Column plane c of a tile: kAdj stages state planes [0,2D) then adjoint planes [0,2D).
-  auto col_plane = [&](int comp) -> const T* {
-    if constexpr (MODE == kAdj) {
-      return comp < 2 * D ? a.jstate + (long long)comp * a.jstride
-                          : a.jadj + (long long)(comp - 2 * D) * a.jstride;
-    } else {
-      return a.jstate + (long long)comp * a.jstride;
-    }
-  };
-
   while (c < c_end) {
     const long long rt_local = c / nJ;
     const int u0 = (int)(c - rt_local * nJ);  // unit range [u0, u1) of this row tile
@@ -371,7 +367,30 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     const int col0 = u0 * kUnitJ, col1 = u1 * kUnitJ;  // column range, multiples of kUnitJ
     const int jt0 = col0 / kTileJ;
     const int jt1 = (col1 + kTileJ - 1) / kTileJ;
-    const int rt = a.row_tile0 + (int)rt_local;
+    // problem this row tile belongs to (uniform per CTA iteration: lives in uniform registers)
+    const long long bc = rt_local / a.tiles_per_problem;
+    const long long prob = a.batch_ids != nullptr ? (long long)a.batch_ids[bc] : bc;
+    const int rt = a.row_tile0 + (int)(rt_local - bc * a.tiles_per_problem);
+    const T* jstate_b = a.jstate + prob * a.bs_j;
+    const T* jadj_b = a.jadj + prob * a.bs_adj;
+    const T* istate_b = MODE == kVel ? a.istate : a.istate + prob * a.bs_j;
+    const T* iadj_b = a.iadj + prob * a.bs_adj;
+    T* out_b = a.out + prob * a.bs_out;
+    T* adj_seed_b = a.adj_seed + prob * a.bs_seed;
+    T* hp0_b = a.hp0 + prob * a.bs_vec;
+    const T* target_b = a.target + prob * a.bs_vec;
+    double* grad_out_b = a.grad_out + prob * a.bs_grad;
+    double* h_part_b = a.h_part + prob * a.bs_part;
+    double* mm_part_b = a.mm_part + prob * a.bs_part;
+    unsigned long long* diverged_b = a.diverged + prob * a.bs_div;
+    // Column plane c of a tile: kAdj stages state planes [0,2D) then adjoint planes [0,2D).
+    auto col_plane = [&](int comp) -> const T* {
+      if constexpr (MODE == kAdj) {
+        return comp < 2 * D ? jstate_b + (long long)comp * a.jstride : jadj_b + (long long)(comp - 2 * D) * a.jstride;
+      } else {
+        return jstate_b + (long long)comp * a.jstride;
+      }
+    };
 
     // ---- row operands --------------------------------------------------------------------
     T ri[R][NR];
@@ -381,10 +400,10 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 #pragma unroll
       for (int k = 0; k < NR; ++k) {
         if constexpr (MODE == kAdj) {
-          ri[r][k] = k < 2 * D ? a.istate[(long long)k * a.istride + row]
-                               : a.iadj[(long long)(k - 2 * D) * a.istride + row];
+          ri[r][k] = k < 2 * D ? istate_b[(long long)k * a.istride + row]
+                               : iadj_b[(long long)(k - 2 * D) * a.istride + row];
         } else {
-          ri[r][k] = a.istate[(long long)k * a.istride + row];
+          ri[r][k] = istate_b[(long long)k * a.istride + row];
         }
       }
     }
@@ -544,13 +563,13 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
               for (int k = 0; k < D; ++k) {
                 const T xn = Math<T>::add_rn(ri[r][k], Math<T>::mul_rn(a.dt, acc[r][k]));
                 ok = ok && Math<T>::finite(xn);
-                a.out[(long long)k * a.ostride + row] = xn;
+                out_b[(long long)k * a.ostride + row] = xn;
               }
               if (!ok)
-                atomicMin(a.diverged, ((unsigned long long)(unsigned)a.step << 32) | (unsigned long long)row);
+                atomicMin(diverged_b, ((unsigned long long)(unsigned)a.step << 32) | (unsigned long long)row);
             } else {
 #pragma unroll
-              for (int k = 0; k < D; ++k) a.out[(long long)k * a.ostride + row] = acc[r][k];
+              for (int k = 0; k < D; ++k) out_b[(long long)k * a.ostride + row] = acc[r][k];
             }
           }
         } else if constexpr (MODE == kFwd) {
@@ -570,33 +589,33 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
                 qn[k] = Math<T>::add_rn(ri[r][k], Math<T>::mul_rn(a.dt, hp[k]));
                 const T pn = Math<T>::add_rn(ri[r][D + k], -Math<T>::mul_rn(a.dt, hq[k]));
                 ok = ok && Math<T>::finite(qn[k]) && Math<T>::finite(pn);
-                a.out[(long long)k * a.ostride + row] = qn[k];
-                a.out[(long long)(D + k) * a.ostride + row] = pn;
+                out_b[(long long)k * a.ostride + row] = qn[k];
+                out_b[(long long)(D + k) * a.ostride + row] = pn;
               }
-              if (!ok) atomicMin(a.diverged, ((unsigned long long)(unsigned)a.step << 32) | 0xffffffffull);
+              if (!ok) atomicMin(diverged_b, ((unsigned long long)(unsigned)a.step << 32) | 0xffffffffull);
               if (a.epi & kEpiFirstStep) {
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                  a.hp0[(long long)k * a.ostride + row] = hp[k];
+                  hp0_b[(long long)k * a.ostride + row] = hp[k];
                   hsum += (double)ri[r][D + k] * (double)hp[k];
                 }
               }
               if (a.epi & kEpiLastStep) {
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                  const T tg = a.target[(long long)k * a.ostride + row];
+                  const T tg = target_b[(long long)k * a.ostride + row];
                   const double df = (double)qn[k] - (double)tg;  // shooting.hpp:324-325
                   msum += df * df;
                   // alpha_T = 2*lambda*(q(1) - target), beta_T = 0   (shooting.hpp:290-296)
-                  a.adj_seed[(long long)k * a.ostride + row] = Math<T>::mul_rn(a.two_lambda, qn[k] - tg);
-                  a.adj_seed[(long long)(D + k) * a.ostride + row] = T(0);
+                  adj_seed_b[(long long)k * a.ostride + row] = Math<T>::mul_rn(a.two_lambda, qn[k] - tg);
+                  adj_seed_b[(long long)(D + k) * a.ostride + row] = T(0);
                 }
               }
             } else {
 #pragma unroll
               for (int k = 0; k < D; ++k) {
-                a.out[(long long)k * a.ostride + row] = hq[k];
-                a.out[(long long)(D + k) * a.ostride + row] = hp[k];
+                out_b[(long long)k * a.ostride + row] = hq[k];
+                out_b[(long long)(D + k) * a.ostride + row] = hp[k];
                 if (a.epi & kEpiFirstStep) hsum += (double)ri[r][D + k] * (double)hp[k];
               }
             }
@@ -611,14 +630,14 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
                 // alpha += dt*d_alpha ; beta += dt*d_beta   (shooting.hpp:302-306)
                 const T an = Math<T>::add_rn(ri[r][2 * D + k], Math<T>::mul_rn(a.dt, da));
                 const T bn = Math<T>::add_rn(ri[r][3 * D + k], Math<T>::mul_rn(a.dt, dbeta));
-                a.out[(long long)k * a.ostride + row] = an;
-                a.out[(long long)(D + k) * a.ostride + row] = bn;
+                out_b[(long long)k * a.ostride + row] = an;
+                out_b[(long long)(D + k) * a.ostride + row] = bn;
                 if (a.epi & kEpiGradOut)  // grad = beta_0 + hp(q0,p0)   (shooting.hpp:311-313)
-                  a.grad_out[row * D + k] =
-                      (double)Math<T>::add_rn(bn, a.hp0[(long long)k * a.ostride + row]);
+                  grad_out_b[row * D + k] =
+                      (double)Math<T>::add_rn(bn, hp0_b[(long long)k * a.ostride + row]);
               } else {
-                a.out[(long long)k * a.ostride + row] = da;
-                a.out[(long long)(D + k) * a.ostride + row] = dbeta;
+                out_b[(long long)k * a.ostride + row] = da;
+                out_b[(long long)(D + k) * a.ostride + row] = dbeta;
               }
             }
           }
@@ -628,11 +647,11 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         // block-uniform flags: every thread takes the same branch around the barriers in block_sum
         if (a.epi & kEpiFirstStep) {
           const double h = block_sum(hsum, red_scratch);
-          if (tid == 0) a.h_part[(long long)rt * R] = h;  // indexed in 128-row units
+          if (tid == 0) h_part_b[(long long)rt * R] = h;  // indexed in 128-row units
         }
         if (a.epi & kEpiLastStep) {
           const double m = block_sum(msum, red_scratch);
-          if (tid == 0) a.mm_part[(long long)rt * R] = m;
+          if (tid == 0) mm_part_b[(long long)rt * R] = m;
         }
       }
     }
@@ -644,43 +663,55 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 // O(N) helpers
 // ---------------------------------------------------------------------------------------------
 
-// Row-major double (n x ncomp) -> ncomp planes of T, cast T(x) as registration.cpp:63 does.
+// Row-major double (n x ncomp) -> ncomp planes of T, cast T(x) as registration.cpp:63 does, for `batch`
+// problems (source stride n*ncomp doubles, destination stride dst_bs elements, divergence word stride div_bs).
 // Non-finite inputs record divergence at `step` (integrate_forward's entry check, shooting.hpp:185-186).
 template <typename T>
-__global__ void aos_to_planes(const double* __restrict__ src, T* __restrict__ dst, long long stride,
-                              int n, int ncomp, unsigned long long* diverged, int step)
+__global__ void aos_to_planes(const double* __restrict__ src, T* __restrict__ dst, long long stride, int n, int ncomp,
+                              unsigned long long* diverged, int step, int batch = 1, long long dst_bs = 0,
+                              long long div_bs = 0, const int* batch_ids = nullptr)
 {
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)n * ncomp) return;
+  const long long per = (long long)n * ncomp;
+  const long long e_all = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e_all >= per * batch) return;
+  const long long bc = e_all / per;
+  const long long b = batch_ids != nullptr ? (long long)batch_ids[bc] : bc;
+  const long long e = e_all - bc * per;
   const int i = (int)(e / ncomp);
   const int c = (int)(e - (long long)i * ncomp);
-  const T v = (T)src[e];
-  dst[(long long)c * stride + i] = v;
+  const T v = (T)src[b * per + e];
+  dst[b * dst_bs + (long long)c * stride + i] = v;
   if (diverged != nullptr && !isfinite(v))
-    atomicMin(diverged, ((unsigned long long)(unsigned)step << 32) | 0xffffffffull);
+    atomicMin(diverged + b * div_bs, ((unsigned long long)(unsigned)step << 32) | 0xffffffffull);
 }
 
 template <typename T>
 __global__ void planes_to_aos(const T* __restrict__ src, long long stride, double* __restrict__ dst, int n,
-                              int ncomp)
+                              int ncomp, int batch = 1, long long src_bs = 0)
 {
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)n * ncomp) return;
+  const long long per = (long long)n * ncomp;
+  const long long e_all = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e_all >= per * batch) return;
+  const long long b = e_all / per;
+  const long long e = e_all - b * per;
   const int i = (int)(e / ncomp);
   const int c = (int)(e - (long long)i * ncomp);
-  dst[e] = (double)src[(long long)c * stride + i];
+  dst[e_all] = (double)src[b * src_bs + (long long)c * stride + i];
 }
 
-// Plane-to-plane copy of the live rows (device-resident snapshot 0 <- bound q0).
+// Plane-to-plane copy of the live rows (device-resident snapshot 0 <- bound q0), per problem.
 template <typename T>
 __global__ void copy_planes(const T* __restrict__ src, long long sstride, T* __restrict__ dst, long long dstride,
-                            int n, int ncomp)
+                            int n, int ncomp, int batch = 1, long long src_bs = 0, long long dst_bs = 0)
 {
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)n * ncomp) return;
+  const long long per = (long long)n * ncomp;
+  const long long e_all = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e_all >= per * batch) return;
+  const long long b = e_all / per;
+  const long long e = e_all - b * per;
   const int c = (int)(e / n);
   const int i = (int)(e - (long long)c * n);
-  dst[(long long)c * dstride + i] = src[(long long)c * sstride + i];
+  dst[b * dst_bs + (long long)c * dstride + i] = src[b * src_bs + (long long)c * sstride + i];
 }
 
 // Finite check of state planes (q0/p0 entry check, shooting.hpp:185-186).
@@ -697,21 +728,24 @@ __global__ void check_finite_planes(const T* __restrict__ src, long long stride,
 }
 
 // scalars[0..2] = {loss, kinetic, mismatch}: fixed ascending sum of the per-row-tile partials
-// (loss = H + lambda*mismatch, shooting.hpp:286-288; H = 1/2 sum_i p_i . hp_i).
+// (loss = H + lambda*mismatch, shooting.hpp:286-288; H = 1/2 sum_i p_i . hp_i).  One block per problem;
+// problem b's partials start at b * n_tiles, its scalars at b * 4 (the 4th word is the divergence record).
 template <int kUnused = 0>
 __global__ void finalize_scalars(const double* __restrict__ h_part, const double* __restrict__ mm_part,
-                                 int n_tiles, double lambda, double* __restrict__ scalars)
+                                 int n_tiles, double lambda, double* __restrict__ scalars,
+                                 const int* batch_ids = nullptr)
 {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  if (threadIdx.x != 0) return;
+  const long long b = batch_ids != nullptr ? (long long)batch_ids[blockIdx.x] : (long long)blockIdx.x;
   double h = 0.0, m = 0.0;
   for (int t = 0; t < n_tiles; ++t) {
-    h += h_part[t];
-    m += mm_part[t];
+    h += h_part[b * n_tiles + t];
+    m += mm_part[b * n_tiles + t];
   }
   h *= 0.5;
-  scalars[1] = h;
-  scalars[2] = m;
-  scalars[0] = h + lambda * m;
+  scalars[b * 4 + 1] = h;
+  scalars[b * 4 + 2] = m;
+  scalars[b * 4 + 0] = h + lambda * m;
 }
 
 // Strictly sequential double sum of squared differences over row-major-equivalent order

@@ -121,9 +121,10 @@ KernelChoice<double> pick_kernel<double, 2, kVel>(int)
 
 // ---- construction ------------------------------------------------------------------------------------
 template <typename T, int D>
-System<T, D>::System(const lms_config& c)
+System<T, D>::System(const lms_config& c, int batch_count)
 {
   cfg = c;
+  batch = std::max(batch_count, 1);
   LMS_CUDA(cudaSetDevice(c.device));
   cudaDeviceProp prop;
   LMS_CUDA(cudaGetDeviceProperties(&prop, c.device));
@@ -149,24 +150,29 @@ System<T, D>::System(const lms_config& c)
   const long long N = (long long)c.n;
   stride_ = std::max<long long>(round_up(N, kRowAlign), kRowAlign);
   const size_t plane = (size_t)stride_;
-  traj_ = dev_alloc_zero<T>((size_t)(max_t_ + 1) * kState * plane);
-  adj_[0] = dev_alloc_zero<T>(kState * plane);
-  adj_[1] = dev_alloc_zero<T>(kState * plane);
-  hp0_ = dev_alloc_zero<T>(D * plane);
-  target_ = dev_alloc_zero<T>(D * plane);
-  q0_ = dev_alloc_zero<T>(D * plane);
+  const size_t B = (size_t)batch;
+  bs_traj_ = (long long)(max_t_ + 1) * kState * stride_;
+  bs_state_ = (long long)kState * stride_;
+  bs_vec_ = (long long)D * stride_;
+  traj_ = dev_alloc_zero<T>(B * (size_t)bs_traj_);
+  adj_[0] = dev_alloc_zero<T>(B * kState * plane);
+  adj_[1] = dev_alloc_zero<T>(B * kState * plane);
+  hp0_ = dev_alloc_zero<T>(B * D * plane);
+  target_ = dev_alloc_zero<T>(B * D * plane);
+  q0_ = dev_alloc_zero<T>(B * D * plane);
   scratch_in_ = dev_alloc_zero<T>(2 * kState * plane);
   scratch_out_ = dev_alloc_zero<T>(kState * plane);
-  d_scalars_ = dev_alloc_zero<double>(4);
+  d_scalars_ = dev_alloc_zero<double>(4 * B);
   d_diverged_ = reinterpret_cast<unsigned long long*>(d_scalars_ + 3);
-  io_cap_ = (size_t)N * D;
+  io_cap_ = (size_t)N * D * B;
   d_io_ = dev_alloc_zero<double>(4 * io_cap_);
-  d_x_ = dev_alloc_zero<double>((size_t)stride_ * D);
-  d_grad_ = dev_alloc_zero<double>((size_t)stride_ * D);
-  LMS_CUDA(cudaMallocHost(&h_scalars_, 4 * sizeof(double)));
+  d_x_ = dev_alloc_zero<double>(std::max((size_t)stride_ * D, B * (size_t)N * D));
+  d_grad_ = dev_alloc_zero<double>(std::max((size_t)stride_ * D, B * (size_t)N * D));
+  d_ids_ = dev_alloc_zero<int>(B);
+  LMS_CUDA(cudaMallocHost(&h_scalars_, 4 * B * sizeof(double)));
   part_tiles_ = (int)(stride_ / kThreads);
-  h_part_ = dev_alloc_zero<double>(part_tiles_);
-  mm_part_ = dev_alloc_zero<double>(part_tiles_);
+  h_part_ = dev_alloc_zero<double>(B * part_tiles_);
+  mm_part_ = dev_alloc_zero<double>(B * part_tiles_);
 }
 
 template <typename T, int D>
@@ -194,6 +200,7 @@ System<T, D>::~System()
   dev_free(d_io_);
   dev_free(d_x_);
   dev_free(d_grad_);
+  dev_free(d_ids_);
   if (h_scalars_) cudaFreeHost(h_scalars_);
   for (auto e : events_) cudaEventDestroy(e);
   if (ev_begin_) cudaEventDestroy(ev_begin_);
@@ -226,11 +233,13 @@ int System<T, D>::row_tile_end_(int bm) const
 
 template <typename T, int D>
 template <int MODE>
-LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_tile0, int row_tiles)
+LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_tile0, int row_tiles,
+                                  int batch_count)
 {
   LaunchPlan p;
   p.bm = kThreads * k.rows_per_thread;
-  p.n_row_tiles = row_tiles >= 0 ? row_tiles : ceil_div(n_rows, p.bm);
+  p.tiles_per_problem = std::max(row_tiles >= 0 ? row_tiles : ceil_div(n_rows, p.bm), 1);
+  p.n_row_tiles = (row_tiles >= 0 ? row_tiles : ceil_div(n_rows, p.bm)) * batch_count;
   p.n_j_tiles = ceil_div((long long)cfg.n, kTileJ);
   (void)row_tile0;
   const long long units_per_row = (long long)p.n_j_tiles * kUnitsPerTile;  // work units, see pair_kernel
@@ -288,6 +297,12 @@ PairArgs<T> System<T, D>::base_args() const
   a.two_lambda = two_lambda_;
   a.epi = kEpiRaw;
   a.step = 0;
+  a.tiles_per_problem = 1;
+  a.batch_ids = nullptr;
+  a.bs_vec = bs_vec_;
+  a.bs_grad = (long long)n() * D;
+  a.bs_part = part_tiles_;
+  a.bs_div = 4;
   return a;
 }
 
@@ -297,6 +312,7 @@ void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchP
 {
   if (plan.grid <= 0) return;
   a.n_row_tiles = plan.n_row_tiles;
+  a.tiles_per_problem = plan.tiles_per_problem;
   a.n_j_tiles = plan.n_j_tiles;
   a.max_seg = plan.max_seg;
   a.partials = partials_;
@@ -309,10 +325,10 @@ void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchP
 // ---- host <-> planes ---------------------------------------------------------------------------------------
 template <typename T, int D>
 void System<T, D>::upload(const double* host, T* planes, long long stride, int count, int ncomp, bool check,
-                          int step)
+                          int step, int batch_count, long long dst_bs)
 {
   if (count <= 0) return;
-  const size_t elems = (size_t)count * ncomp;
+  const size_t elems = (size_t)count * ncomp * batch_count;
   if (elems > io_cap_) {
     sync();
     dev_free(d_io_);
@@ -322,7 +338,7 @@ void System<T, D>::upload(const double* host, T* planes, long long stride, int c
   LMS_CUDA(cudaMemcpyAsync(d_io_, host, elems * sizeof(double), cudaMemcpyHostToDevice, stream_));
   const int blocks = ceil_div((long long)elems, 256);
   aos_to_planes<T><<<blocks, 256, 0, stream_>>>(d_io_, planes, stride, count, ncomp, check ? d_diverged_ : nullptr,
-                                                step);
+                                                step, batch_count, dst_bs, 4);
   LMS_CUDA(cudaGetLastError());
 }
 
@@ -364,10 +380,17 @@ void System<T, D>::read_diverged_or_throw()
   }
 }
 
+template <typename T, int D>
+void System<T, D>::require_single(const char* what) const
+{
+  if (batch != 1) throw StatusError{LMS_ERR_STATE, what};
+}
+
 // ---- HamiltonianSystem members ----------------------------------------------------------------------------------
 template <typename T, int D>
 void System<T, D>::derivatives(const double* q, const double* p, double* hq, double* hp)
 {
+  require_single("per-function calls need a single-problem handle");
   if (n() == 0) return;
   upload(q, scratch_in_, stride_, n(), D, false, 0);
   upload(p, scratch_in_ + D * stride_, stride_, n(), D, false, 0);
@@ -386,6 +409,7 @@ void System<T, D>::derivatives(const double* q, const double* p, double* hq, dou
 template <typename T, int D>
 void System<T, D>::hamiltonian(const double* q, const double* p, double* out)
 {
+  require_single("per-function calls need a single-problem handle");
   *out = 0.0;
   if (n() == 0) return;
   upload(q, scratch_in_, stride_, n(), D, false, 0);
@@ -409,6 +433,7 @@ template <typename T, int D>
 void System<T, D>::adjoint_step(const double* q, const double* p, const double* alpha, const double* beta,
                                 double* da, double* db)
 {
+  require_single("per-function calls need a single-problem handle");
   if (n() == 0) return;
   upload(q, scratch_in_, stride_, n(), D, false, 0);
   upload(p, scratch_in_ + D * stride_, stride_, n(), D, false, 0);
@@ -430,6 +455,7 @@ void System<T, D>::adjoint_step(const double* q, const double* p, const double* 
 template <typename T, int D>
 void System<T, D>::mismatch_sq(const double* a, const double* b, double* out)
 {
+  require_single("per-function calls need a single-problem handle");
   *out = 0.0;
   if (n() == 0) return;
   upload(a, scratch_in_, stride_, n(), D, false, 0);
@@ -445,6 +471,7 @@ void System<T, D>::mismatch_sq(const double* a, const double* b, double* out)
 template <typename T, int D>
 void System<T, D>::integrate_forward(const double* q0, const double* p0, int timesteps, double* tq, double* tp)
 {
+  require_single("per-function calls need a single-problem handle");
   if (timesteps < 1) throw StatusError{LMS_ERR_INVALID, "timesteps must be >= 1"};
   if (timesteps > max_t_) throw StatusError{LMS_ERR_INVALID, "timesteps exceeds cfg.max_timesteps"};
   if (comm_active_) throw StatusError{LMS_ERR_STATE, "integrate_forward is single-GPU; use the bound objective"};
@@ -484,35 +511,42 @@ void System<T, D>::integrate_forward(const double* q0, const double* p0, int tim
 }
 
 // ---- the bound objective ----------------------------------------------------------------------------------------
+// q0 / target: batch x n x D (one registration per problem; batch == 1 for the plain handle).
 template <typename T, int D>
 void System<T, D>::bind(const double* q0, const double* target, double lambda_in, int timesteps_in)
 {
   if (timesteps_in < 1) throw StatusError{LMS_ERR_INVALID, "timesteps must be >= 1"};
   if (timesteps_in > max_t_) throw StatusError{LMS_ERR_INVALID, "timesteps exceeds cfg.max_timesteps"};
   if (!(lambda_in >= 0)) throw StatusError{LMS_ERR_INVALID, "lambda must be >= 0"};
+  if (batch > 1 && comm_active_) throw StatusError{LMS_ERR_STATE, "batches are not row-partitioned"};
   sync();
   destroy_graph();
   bound = false;
   lambda = lambda_in;
   timesteps = timesteps_in;
-  host_q0.assign(q0, q0 + (size_t)n() * D);
-  host_target.assign(target, target + (size_t)n() * D);
+  const size_t per = (size_t)n() * D;
+  host_q0.assign(q0, q0 + per * batch);
+  host_target.assign(target, target + per * batch);
   dt_ = T(1.0 / timesteps);              // shooting.hpp:190,196,298
   two_lambda_ = T(2) * T(lambda);        // shooting.hpp:293
   q0_bad_ = false;
-  for (double v : host_q0)
-    if (!std::isfinite((double)(T)v)) q0_bad_ = true;
+  q0_bad_problem_.assign(batch, 0);
+  for (size_t e = 0; e < host_q0.size(); ++e)
+    if (!std::isfinite((double)(T)host_q0[e])) {
+      q0_bad_ = true;
+      q0_bad_problem_[e / std::max<size_t>(per, 1)] = 1;
+    }
   traj0_is_q0_ = false;
   stored_t_ = -1;
   if (n() > 0) {
-    upload(q0, q0_, stride_, n(), D, false, 0);
-    upload(target, target_, stride_, n(), D, false, 0);
+    upload(q0, q0_, stride_, n(), D, false, 0, batch, bs_vec_);
+    upload(target, target_, stride_, n(), D, false, 0, batch, bs_vec_);
     const int tb_f = row_tile_begin_(kThreads * k_fwd_.rows_per_thread);
     const int te_f = row_tile_end_(kThreads * k_fwd_.rows_per_thread);
     const int tb_a = row_tile_begin_(kThreads * k_adj_.rows_per_thread);
     const int te_a = row_tile_end_(kThreads * k_adj_.rows_per_thread);
-    plan_fwd_ = plan_for<kFwd>(k_fwd_, n(), tb_f, std::max(te_f - tb_f, 0));
-    plan_adj_ = plan_for<kAdj>(k_adj_, n(), tb_a, std::max(te_a - tb_a, 0));
+    plan_fwd_ = plan_for<kFwd>(k_fwd_, n(), tb_f, std::max(te_f - tb_f, 0), batch);
+    plan_adj_ = plan_for<kAdj>(k_adj_, n(), tb_a, std::max(te_a - tb_a, 0), batch);
     ensure_partials(std::max(plan_fwd_.partial_elems, plan_adj_.partial_elems),
                     std::max(plan_fwd_.n_row_tiles, plan_adj_.n_row_tiles));
     sync();
@@ -538,12 +572,19 @@ void System<T, D>::bind(const double* q0, const double* target, double lambda_in
   bound = true;
 }
 
-// Enqueue one objective evaluation on stream_: x (double, in d_x_) -> scalars in d_scalars_, grad in d_grad_.
+// Enqueue one objective evaluation on stream_ for `count` problems (ids on the device, or all): x (double, in
+// d_x_) -> scalars in d_scalars_, grad in d_grad_.
 template <typename T, int D>
-void System<T, D>::enqueue_eval(bool timed)
+void System<T, D>::enqueue_eval(bool timed, int count, const int* d_ids)
 {
   last_eval_launches = 0;
   const int Tn = timesteps;
+  if (count < 0) count = batch;
+  LaunchPlan pf = plan_fwd_, pa = plan_adj_;
+  if (count != batch) {  // a subset of the batch: same kernels, fewer row tiles
+    pf = plan_for<kFwd>(k_fwd_, n(), 0, plan_fwd_.tiles_per_problem, count);
+    pa = plan_for<kAdj>(k_adj_, n(), 0, plan_adj_.tiles_per_problem, count);
+  }
   if (timed && (int)events_.size() < 4 * Tn) {
     while ((int)events_.size() < 4 * Tn) {
       cudaEvent_t e;
@@ -552,15 +593,23 @@ void System<T, D>::enqueue_eval(bool timed)
     }
   }
   int ev = 0;
-  reset_diverged();
+  // reset every problem's divergence word (the 4th double of its scalar record) -- small strided memset
+  LMS_CUDA(cudaMemset2DAsync(d_diverged_, 4 * sizeof(double), 0xff, sizeof(unsigned long long), batch, stream_));
   {
     // p0[i][c] = T(x[i*D+c])  (registration.cpp:61-63); non-finite p0 -> DivergedError(0) (shooting.hpp:185-186)
-    const long long elems = (long long)n() * D;
+    const long long elems = (long long)n() * D * count;
     aos_to_planes<T><<<ceil_div(elems, 256), 256, 0, stream_>>>(d_x_, snapshot(0) + D * stride_, stride_, n(), D,
-                                                                d_diverged_, 0);
+                                                                d_diverged_, 0, count, bs_traj_, 4, d_ids);
     LMS_CUDA(cudaGetLastError());
     ++last_eval_launches;
   }
+  auto batch_strides = [&](PairArgs<T>& a, long long bs_out, long long bs_adj) {
+    a.batch_ids = d_ids;
+    a.bs_j = bs_traj_;
+    a.bs_adj = bs_adj;
+    a.bs_out = bs_out;
+    a.bs_seed = bs_state_;
+  };
   // forward Euler flow, T+1 snapshots kept for the adjoint (shooting.hpp:199-212)
   for (int t = 0; t < Tn; ++t) {
     PairArgs<T> a = base_args();
@@ -570,8 +619,9 @@ void System<T, D>::enqueue_eval(bool timed)
     a.row_tile0 = row_tile_begin_(plan_fwd_.bm);
     a.epi = kEpiEuler | (t == 0 ? kEpiFirstStep : 0u) | (t == Tn - 1 ? kEpiLastStep : 0u);
     a.step = t + 1;
+    batch_strides(a, bs_traj_, 0);
     if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
-    launch<kFwd>(k_fwd_, a, plan_fwd_);
+    launch<kFwd>(k_fwd_, a, pf);
     if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
     if (comm_active_) {
       all_gather_state(snapshot(t + 1));
@@ -582,7 +632,7 @@ void System<T, D>::enqueue_eval(bool timed)
     all_gather_doubles(h_part_);
     all_gather_doubles(mm_part_);
   }
-  finalize_scalars<0><<<1, 32, 0, stream_>>>(h_part_, mm_part_, part_tiles_, lambda, d_scalars_);
+  finalize_scalars<0><<<count, 32, 0, stream_>>>(h_part_, mm_part_, part_tiles_, lambda, d_scalars_, d_ids);
   LMS_CUDA(cudaGetLastError());
   ++last_eval_launches;
   // discrete adjoint sweep t = T-1 .. 0 (shooting.hpp:300-307), final gradient fused into the t = 0 launch
@@ -595,8 +645,9 @@ void System<T, D>::enqueue_eval(bool timed)
     a.row_tile0 = row_tile_begin_(plan_adj_.bm);
     a.epi = kEpiEuler | (t == 0 ? kEpiGradOut : 0u);
     a.step = t;
+    batch_strides(a, bs_state_, bs_state_);
     if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
-    launch<kAdj>(k_adj_, a, plan_adj_);
+    launch<kAdj>(k_adj_, a, pa);
     if (timed) LMS_CUDA(cudaEventRecord(events_[ev++], stream_));
     if (comm_active_ && t > 0) all_gather_state(adj_[cur ^ 1]);
     cur ^= 1;
@@ -611,9 +662,81 @@ void System<T, D>::enqueue_eval(bool timed)
   final_adj_ = cur;
 }
 
+// Shared body of eval / eval_batch: copies x in, runs the evaluation, copies grad and the scalar records out.
+template <typename T, int D>
+void System<T, D>::eval_batch(const double* x, double* grad, double* scalars, int* diverged_step, int count,
+                              const int* ids)
+{
+  if (!bound) throw StatusError{LMS_ERR_STATE, "lms_bind_registration must precede evaluation"};
+  if (count < 0 || count > batch) throw StatusError{LMS_ERR_INVALID, "bad problem count"};
+  const bool subset = ids != nullptr;
+  if (!subset) count = batch;
+  for (int b = 0; b < batch; ++b)
+    if (!subset && diverged_step) diverged_step[b] = -1;
+  if (n() == 0 || count == 0) {
+    for (int k = 0; k < count; ++k) {
+      const int b = subset ? ids[k] : k;
+      scalars[3 * b] = scalars[3 * b + 1] = scalars[3 * b + 2] = 0.0;
+      if (diverged_step) diverged_step[b] = -1;
+    }
+    return;
+  }
+  const size_t per = (size_t)n() * D;
+  if (!traj0_is_q0_) {
+    const long long elems = (long long)per * batch;
+    copy_planes<T><<<ceil_div(elems, 256), 256, 0, stream_>>>(q0_, stride_, snapshot(0), stride_, n(), D, batch,
+                                                              bs_vec_, bs_traj_);
+    LMS_CUDA(cudaGetLastError());
+    traj0_is_q0_ = true;
+  }
+  if (subset) {
+    for (int k = 0; k < count; ++k) {
+      if (ids[k] < 0 || ids[k] >= batch) throw StatusError{LMS_ERR_INVALID, "problem id out of range"};
+      LMS_CUDA(cudaMemcpyAsync(d_x_ + ids[k] * per, x + ids[k] * per, per * sizeof(double), cudaMemcpyHostToDevice,
+                               stream_));
+    }
+    LMS_CUDA(cudaMemcpyAsync(d_ids_, ids, count * sizeof(int), cudaMemcpyHostToDevice, stream_));
+  } else {
+    LMS_CUDA(cudaMemcpyAsync(d_x_, x, per * batch * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  }
+  LMS_CUDA(cudaEventRecord(ev_begin_, stream_));
+  if (graph_ && !subset && !kernel_timing) {
+    LMS_CUDA(cudaGraphLaunch(graph_, stream_));
+    last_eval_launches = graph_launches_;
+  } else {
+    enqueue_eval(false, count, subset ? d_ids_ : nullptr);
+  }
+  LMS_CUDA(cudaEventRecord(ev_end_, stream_));
+  if (subset) {
+    for (int k = 0; k < count; ++k)
+      LMS_CUDA(cudaMemcpyAsync(grad + ids[k] * per, d_grad_ + ids[k] * per, per * sizeof(double),
+                               cudaMemcpyDeviceToHost, stream_));
+  } else {
+    LMS_CUDA(cudaMemcpyAsync(grad, d_grad_, per * batch * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  }
+  LMS_CUDA(cudaMemcpyAsync(h_scalars_, d_scalars_, 4 * sizeof(double) * batch, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  stored_t_ = timesteps;
+  float ms = 0.f;
+  LMS_CUDA(cudaEventElapsedTime(&ms, ev_begin_, ev_end_));
+  last_eval_ms = ms;
+  for (int k = 0; k < count; ++k) {
+    const int b = subset ? ids[k] : k;
+    unsigned long long word;
+    std::memcpy(&word, h_scalars_ + 4 * b + 3, sizeof(word));
+    int step = word == kNotDiverged ? -1 : (int)(word >> 32);
+    if (q0_bad_problem_[b]) step = 0;  // non-finite template: DivergedError(0), shooting.hpp:185-186
+    if (diverged_step) diverged_step[b] = step;
+    scalars[3 * b] = h_scalars_[4 * b];
+    scalars[3 * b + 1] = h_scalars_[4 * b + 1];
+    scalars[3 * b + 2] = h_scalars_[4 * b + 2];
+  }
+}
+
 template <typename T, int D>
 void System<T, D>::eval(const double* x, double* grad, double* scalars, bool device_ptrs)
 {
+  require_single("this handle holds a batch: use lms_batch_eval");
   if (!bound) throw StatusError{LMS_ERR_STATE, "lms_bind_registration must precede evaluation"};
   if (n() == 0) {
     scalars[0] = scalars[1] = scalars[2] = 0.0;
@@ -667,9 +790,30 @@ void System<T, D>::eval(const double* x, double* grad, double* scalars, bool dev
 template <typename T, int D>
 void System<T, D>::final_q(double* out)
 {
+  require_single("this handle holds a batch: use lms_batch_final_q");
   if (stored_t_ < 0) throw StatusError{LMS_ERR_STATE, "no stored trajectory"};
   if (n() == 0) return;
   download(snapshot(stored_t_), stride_, out, n(), D);
+  sync();
+}
+
+// q(1) of every problem of the batch: batch x n x D.
+template <typename T, int D>
+void System<T, D>::final_q_batch(double* out)
+{
+  if (stored_t_ < 0) throw StatusError{LMS_ERR_STATE, "no stored trajectory"};
+  if (n() == 0) return;
+  const size_t elems = (size_t)n() * D * batch;
+  if (elems > io_cap_) {
+    sync();
+    dev_free(d_io_);
+    io_cap_ = elems;
+    d_io_ = dev_alloc_zero<double>(4 * io_cap_);
+  }
+  planes_to_aos<T><<<ceil_div((long long)elems, 256), 256, 0, stream_>>>(snapshot(stored_t_), stride_, d_io_ + io_cap_,
+                                                                         n(), D, batch, bs_traj_);
+  LMS_CUDA(cudaGetLastError());
+  LMS_CUDA(cudaMemcpyAsync(out, d_io_ + io_cap_, elems * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   sync();
 }
 
@@ -692,6 +836,7 @@ void System<T, D>::ensure_points(size_t m)
 template <typename T, int D>
 void System<T, D>::velocities(const double* q, const double* p, size_t m, const double* pts, double* out)
 {
+  require_single("per-function calls need a single-problem handle");
   if (m == 0) return;
   ensure_points(m);
   if (n() > 0) {
@@ -721,6 +866,7 @@ void System<T, D>::velocities(const double* q, const double* p, size_t m, const 
 template <typename T, int D>
 void System<T, D>::warp_stored(size_t m, const double* pts, double* out)
 {
+  require_single("per-function calls need a single-problem handle");
   if (stored_t_ < 1) throw StatusError{LMS_ERR_STATE, "no stored trajectory: integrate or evaluate first"};
   if (m == 0) return;
   ensure_points(m);
@@ -841,11 +987,12 @@ const char* variant_name(int precision, int variant)
   return pick_kernel<double, 3, kFwd>(variant).name;
 }
 
-SystemBase* create_system(const lms_config& cfg)
+SystemBase* create_system(const lms_config& cfg, int batch_count)
 {
   const bool f32 = cfg.precision == LMS_PRECISION_F32;
-  if (cfg.dim == 3) return f32 ? (SystemBase*)new System<float, 3>(cfg) : (SystemBase*)new System<double, 3>(cfg);
-  return f32 ? (SystemBase*)new System<float, 2>(cfg) : (SystemBase*)new System<double, 2>(cfg);
+  if (cfg.dim == 3)
+    return f32 ? (SystemBase*)new System<float, 3>(cfg, batch_count) : (SystemBase*)new System<double, 3>(cfg, batch_count);
+  return f32 ? (SystemBase*)new System<float, 2>(cfg, batch_count) : (SystemBase*)new System<double, 2>(cfg, batch_count);
 }
 
 }  // namespace lms

@@ -55,6 +55,11 @@ class SystemBase {
   virtual void velocities(const double* q, const double* p, size_t m, const double* pts, double* out) = 0;
   virtual void warp_stored(size_t m, const double* pts, double* out) = 0;
   virtual void comm_init(const unsigned char* id, int rank, int world) = 0;
+  // population batches: `count` problems listed in ids (all when ids == nullptr); arrays are full-batch sized
+  virtual void eval_batch(const double* x, double* grad, double* scalars, int* diverged_step, int count,
+                          const int* ids) = 0;
+  virtual void final_q_batch(double* out) = 0;
+  int batch = 1;
 
   lms_config cfg{};
   int last_diverged_step = -1;
@@ -98,6 +103,7 @@ struct LaunchPlan {
   int max_seg = 1;
   int n_row_tiles = 0;
   int n_j_tiles = 0;
+  int tiles_per_problem = 1;
   int bm = 0;
   size_t partial_elems = 0;
 };
@@ -105,7 +111,7 @@ struct LaunchPlan {
 template <typename T, int D>
 class System final : public SystemBase {
  public:
-  explicit System(const lms_config& c);
+  System(const lms_config& c, int batch_count);
   ~System() override;
 
   void hamiltonian(const double* q, const double* p, double* out) override;
@@ -120,6 +126,9 @@ class System final : public SystemBase {
   void velocities(const double* q, const double* p, size_t m, const double* pts, double* out) override;
   void warp_stored(size_t m, const double* pts, double* out) override;
   void comm_init(const unsigned char* id, int rank, int world) override;
+  void eval_batch(const double* x, double* grad, double* scalars, int* diverged_step, int count,
+                  const int* ids) override;
+  void final_q_batch(double* out) override;
 
  private:
   static constexpr int kState = 2 * D;  // planes per (q,p) or (alpha,beta) state
@@ -128,18 +137,21 @@ class System final : public SystemBase {
   int n() const { return (int)cfg.n; }
 
   template <int MODE>
-  LaunchPlan plan_for(const KernelChoice<T>& k, int n_rows, int row_tile0 = -1, int row_tiles = -1);
+  LaunchPlan plan_for(const KernelChoice<T>& k, int n_rows, int row_tile0 = -1, int row_tiles = -1,
+                      int batch_count = 1);
   template <int MODE>
   void launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchPlan& plan);
   void ensure_partials(size_t elems, int row_tiles);
   PairArgs<T> base_args() const;
 
-  void upload(const double* host, T* planes, long long stride, int count, int ncomp, bool check, int step);
+  void upload(const double* host, T* planes, long long stride, int count, int ncomp, bool check, int step,
+              int batch_count = 1, long long dst_bs = 0);
   void download(const T* planes, long long stride, double* host, int count, int ncomp);
   void reset_diverged();
   void read_diverged_or_throw();
   void sync() { LMS_CUDA(cudaStreamSynchronize(stream_)); }
-  void enqueue_eval(bool timed);
+  void enqueue_eval(bool timed, int count = -1, const int* d_ids = nullptr);
+  void require_single(const char* what) const;
   void destroy_graph();
   void ensure_points(size_t m);
   void all_gather_state(T* state_planes);
@@ -148,7 +160,11 @@ class System final : public SystemBase {
   cudaStream_t stream_ = nullptr;
   int num_sms_ = 0;
   long long stride_ = 0;
+  long long bs_traj_ = 0;   // elements between consecutive problems' trajectories
+  long long bs_state_ = 0;  // ... between their (alpha,beta) states
+  long long bs_vec_ = 0;    // ... between their D-plane vectors (hp0, target, q0)
   int max_t_ = 0;
+  int* d_ids_ = nullptr;
   T inv_sig2_{}, kexp_{};
 
   KernelChoice<T> k_fwd_, k_adj_, k_vel_;
@@ -181,6 +197,7 @@ class System final : public SystemBase {
   // bound problem
   T dt_{}, two_lambda_{};
   bool q0_bad_ = false;
+  std::vector<char> q0_bad_problem_;
   bool traj0_is_q0_ = false;
   int stored_t_ = -1;  // timesteps of the trajectory currently in traj_ (-1: none)
   int final_adj_ = 0;  // which adj_ buffer holds (alpha_0, beta_0) after an eval
@@ -206,7 +223,7 @@ struct RowPartition {
 };
 RowPartition partition_rows(long long n, int world, int rank);
 
-SystemBase* create_system(const lms_config& cfg);
+SystemBase* create_system(const lms_config& cfg, int batch_count = 1);
 const char* variant_name(int precision, int variant);
 
 }  // namespace lms

@@ -1,0 +1,107 @@
+"""GPU tests of the population-batch path (lms_batch_*): many independent registrations per launch."""
+import numpy as np
+import pytest
+
+from conftest import rel_inf
+
+pytestmark = pytest.mark.gpu
+SIGMA = 1.5
+TOL = {"f64": 1e-10, "f32": 1e-5}
+
+
+def make_batch(batch, n, seed, dim=3):
+    rng = np.random.default_rng(seed)
+    q0 = rng.uniform(-7, 7, (batch, n, dim))
+    p0 = 0.75 * rng.normal(size=(batch, n, dim))
+    target = q0 + 0.5 * rng.normal(size=(batch, n, dim))
+    return q0, p0, target
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("batch,n", [(1, 300), (5, 257), (12, 600), (40, 100)])
+def test_batched_evaluation_matches_oracle_per_problem(oracle, prec, batch, n):
+    from paper_1907_04839_b200 import BatchedRegistrations
+
+    T, lam = 5, 10.0
+    q0, p0, target = make_batch(batch, n, 100 + batch)
+    br = BatchedRegistrations(SIGMA, n, batch, 3, prec, max_timesteps=T)
+    br.bind(q0, target, lam, T)
+    scalars, grad, div = br.evaluate(p0)
+    finals = br.final_q()
+    assert (div == -1).all()
+    for b in range(batch):
+        loss, kin, mm, g = oracle.compute_gradient(prec, q0[b], p0[b], target[b], SIGMA, lam, T)
+        assert scalars[b, 0] == pytest.approx(loss, rel=TOL[prec])
+        assert scalars[b, 1] == pytest.approx(kin, rel=TOL[prec])
+        assert scalars[b, 2] == pytest.approx(mm, rel=TOL[prec])
+        assert rel_inf(grad[b], g) <= TOL[prec]
+        assert rel_inf(finals[b], oracle.integrate_forward(prec, q0[b], p0[b], SIGMA, T)[0][-1]) <= TOL[prec]
+    # deterministic, and a second evaluation reuses the captured graph
+    again = br.evaluate(p0)
+    assert np.array_equal(again[0], scalars) and np.array_equal(again[1], grad)
+    br.close()
+
+
+def test_subset_evaluation_and_isolated_divergence(oracle):
+    from paper_1907_04839_b200 import BatchedRegistrations
+
+    batch, n, T, lam = 7, 200, 4, 10.0
+    q0, p0, target = make_batch(batch, n, 9)
+    br = BatchedRegistrations(SIGMA, n, batch, 3, "f64", max_timesteps=T)
+    br.bind(q0, target, lam, T)
+    full = br.evaluate(p0)
+    ids = [5, 1, 3]
+    sub = br.evaluate(p0, ids)
+    for b in range(batch):
+        if b in ids:
+            assert np.allclose(sub[0][b], full[0][b], rtol=1e-13) and rel_inf(sub[1][b], full[1][b]) <= 1e-12
+        else:
+            assert not sub[0][b].any() and not sub[1][b].any()
+    bad = p0.copy()
+    bad[2, 7, 1] = np.nan
+    scalars, grad, div = br.evaluate(bad)
+    assert div[2] == 0 and (np.delete(div, 2) == -1).all()  # DivergedError(0) for problem 2 only
+    for b in (0, 1, 3, 4, 5, 6):
+        assert np.array_equal(scalars[b], full[0][b]) and np.array_equal(grad[b], full[1][b])
+    br.close()
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_batched_registrations_match_single_runs(prec):
+    from paper_1907_04839_b200 import BatchedRegistrations, LbfgsParams, ShootingConfig, register_landmarks
+
+    batch, n, T, lam, iters = 6, 300, 5, 1e3, 12
+    q0, _, target = make_batch(batch, n, 21)
+    br = BatchedRegistrations(SIGMA, n, batch, 3, prec, max_timesteps=T)
+    br.bind(q0, target, lam, T)
+    res = br.register(LbfgsParams(max_iter=iters))
+    br.close()
+    assert (res.status == 0).all()
+    # rounds ~ the longest single run, not the sum over problems: the calls really are coalesced
+    assert res.rounds <= res.evaluations.max() + 1 and res.rounds < res.evaluations.sum()
+    for b in range(batch):
+        one = register_landmarks(q0[b], target[b], ShootingConfig(sigma=SIGMA, timesteps=T, lam=lam, max_iter=iters,
+                                                                  precision=prec))
+        assert res.initial_loss[b] == pytest.approx(one.initial_loss, rel=TOL[prec])
+        if prec == "f64":
+            assert res.iterations[b] == one.iterations and res.evaluations[b] == one.evaluations
+            assert res.final_loss[b] == pytest.approx(one.final_loss, rel=1e-8)
+            assert np.abs(res.warped[b] - one.warped).max() <= 1e-6
+        else:
+            assert np.abs(res.warped[b] - one.warped).max() <= 5e-3
+        assert res.final_loss[b] < res.initial_loss[b]
+
+
+def test_batch_handle_rejects_single_problem_calls():
+    from paper_1907_04839_b200 import BatchedRegistrations, StateError, _lib
+    import ctypes
+
+    br = BatchedRegistrations(SIGMA, 50, 3, 3, "f64", max_timesteps=3)
+    q = np.zeros((50, 3))
+    out = ctypes.c_double()
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = br.lib.lms_hamiltonian(br.handle, q.ctypes.data_as(dp), q.ctypes.data_as(dp), ctypes.byref(out))
+    with pytest.raises(StateError):
+        _lib.check(rc, br.handle)
+    assert br.lib.lms_batch_size(br.handle) == 3
+    br.close()
