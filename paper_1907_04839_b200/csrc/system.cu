@@ -249,7 +249,9 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kThreads, 0));
   per_sm = std::max(per_sm, 1);
   const long long full = (long long)num_sms_ * per_sm;
-  // never more CTAs than staged tiles: a CTA should sweep at least one full tile's worth of columns
+  // Never more CTAs than staged tiles: a CTA sweeps at least one full tile's worth of columns.  (Measured:
+  // going finer -- 32 columns per CTA -- makes N = 1000..2000 slower, 0.30 -> 0.43 ms and 0.35 -> 0.88 ms per
+  // gradient: the partial-slot write / fence / counter / re-read chain costs more than the extra parallelism.)
   p.grid = (int)std::min<long long>(full, std::max<long long>(cells / kUnitsPerTile, 1));
   const long long per_cta = (cells + p.grid - 1) / p.grid;
   p.max_seg = (int)((per_cta + units_per_row - 1) / units_per_row) + 1;
