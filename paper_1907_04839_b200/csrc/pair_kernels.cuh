@@ -73,7 +73,7 @@ struct PairArgs {
   int* counters;
   int max_seg;
   // constants, rounded on the host exactly as the reference rounds them (shooting.hpp:63-68,114-115,
-  // 196,293): kexp = k_scale * log2(e) for float (ex2.approx), k_scale itself for double.
+  // 196,293): kexp = k_scale * log2(e) for float (ex2.approx), k_scale * log2(e) * 16 for double (Math<double>).
   T kexp;
   T inv_sig2;
   T dt;
@@ -96,7 +96,7 @@ struct Math;
 
 template <>
 struct Math<float> {
-  static __device__ __forceinline__ float kernel(float r2, float kexp)
+  static __device__ __forceinline__ float kernel(float r2, float kexp, const double* = nullptr)
   {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(r2 * kexp));
@@ -107,9 +107,42 @@ struct Math<float> {
   static __device__ __forceinline__ bool finite(float a) { return isfinite(a); }
 };
 
+// 2^(j/16), j = 0..15, correctly rounded (generated with 60-digit decimal arithmetic).
+__device__ __constant__ double kExp2Table[16] = {
+    0x1.0000000000000p+0, 0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0, 0x1.2387a6e756238p+0,
+    0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0, 0x1.4bfdad5362a27p+0, 0x1.5ab07dd485429p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0, 0x1.9c49182a3f090p+0,
+    0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0, 0x1.ea4afa2a490dap+0};
+
 template <>
 struct Math<double> {
-  static __device__ __forceinline__ double kernel(double r2, double kexp) { return exp(r2 * kexp); }
+  // exp(r2 * k_scale) for r2 * k_scale <= 0, branch-free.  kexp = k_scale * log2(e) * 16 (host, one
+  // rounding), s = r2 * kexp; 2^(s/16) = 2^n * 2^(j/16) * 2^(g/16) with 16 n + j = rint(s), g = s - rint(s)
+  // in [-1/2, 1/2]: a 16-entry shared-memory table (16 x 8 B spans the 32 banks exactly once: conflict-free
+  // for any index pattern) and a degree-7 polynomial (truncation 1.2e-18).  13 DP-pipe operations against
+  // the 18 of CUDA's exp(), and no slow path: with landmarks many sigma apart most pairs underflow, which
+  // is exactly where the library routine branches.  Results below the normal range flush to zero.
+  static __device__ __forceinline__ double kernel(double r2, double kexp, const double* __restrict__ tbl)
+  {
+    double s = r2 * kexp;
+    s = s < -17280.0 ? -17280.0 : s;  // 2^-1080; a NaN argument falls through and propagates
+    const double magic = 6755399441055744.0;  // 1.5 * 2^52: the low word of (s + magic) is rint(s)
+    const double km = __dadd_rn(s, magic);
+    const int ki = __double2loint(km);
+    const double g = s - __dadd_rn(km, -magic);
+    double p = 0x1.ffcbfc588b0c7p-45;          // (ln2/16)^k / k!, k = 7 .. 1
+    p = fma(p, g, 0x1.430912f86c787p-37);
+    p = fma(p, g, 0x1.5d87fe78a6731p-30);
+    p = fma(p, g, 0x1.3b2ab6fba4e77p-23);
+    p = fma(p, g, 0x1.c6b08d704a0c0p-17);
+    p = fma(p, g, 0x1.ebfbdff82c58fp-11);
+    p = fma(p, g, 0x1.62e42fefa39efp-5);
+    p = fma(p, g, 1.0);
+    const double r = tbl[ki & 15] * p;
+    const int n = ki >> 4;
+    const double scaled = __hiloint2double(__double2hiint(r) + n * 1048576, __double2loint(r));
+    return n < -1021 ? 0.0 : scaled;
+  }
   static __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
   static __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
   static __device__ __forceinline__ bool finite(double a) { return isfinite(a); }
@@ -128,7 +161,7 @@ struct Shape {
 //   with t = inv_sig2 (dx.db);  d_alpha = inv_sig2 * acc[0..D),  d_beta = acc[D..2D).
 template <typename T, int D, int MODE>
 __device__ __forceinline__ void pair_term(const T* __restrict__ ri, const T* __restrict__ cj,
-                                          T* __restrict__ acc, T kexp, T inv_sig2)
+                                          T* __restrict__ acc, T kexp, T inv_sig2, const double* __restrict__ tbl)
 {
   T dx[D];
 #pragma unroll
@@ -136,7 +169,7 @@ __device__ __forceinline__ void pair_term(const T* __restrict__ ri, const T* __r
   T r2 = dx[0] * dx[0];
 #pragma unroll
   for (int c = 1; c < D; ++c) r2 = fma(dx[c], dx[c], r2);
-  const T k = Math<T>::kernel(r2, kexp);
+  const T k = Math<T>::kernel(r2, kexp, tbl);
   if constexpr (MODE == kVel) {
 #pragma unroll
     for (int c = 0; c < D; ++c) acc[c] = fma(k, cj[D + c], acc[c]);
@@ -347,7 +380,12 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 
   __shared__ __align__(16) T tile[2][NC][kTileJ];
   __shared__ double red_scratch[kThreads];
+  __shared__ double exp_tbl[16];  // fp64 only: 2^(j/16) for Math<double>::kernel
   __shared__ int s_last;
+  if constexpr (sizeof(T) == 8) {
+    if (threadIdx.x < 16) exp_tbl[threadIdx.x] = kExp2Table[threadIdx.x];
+    __syncthreads();
+  }
 
   const int tid = threadIdx.x;
   // Work is counted in units of kUnitJ columns of one row tile, so every CTA's share differs by at most
@@ -466,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 #pragma unroll
           for (int u = 0; u < JU; ++u)
 #pragma unroll
-            for (int r = 0; r < R; ++r) pair_term<T, D, MODE>(ri[r], cj[u], acc[r], a.kexp, a.inv_sig2);
+            for (int r = 0; r < R; ++r) pair_term<T, D, MODE>(ri[r], cj[u], acc[r], a.kexp, a.inv_sig2, exp_tbl);
         } else {
 #pragma unroll
           for (int u = 0; u < JU; ++u) {
