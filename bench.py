@@ -39,7 +39,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
-    ap.add_argument("--n", type=int, default=0, help="landmarks (default: 20000 at 1 GPU, 200000 at >1)")
+    ap.add_argument("--landmarks", "--n", dest="n", type=int, default=0, help="landmarks (default: 20000 at 1 GPU, 200000 at >1)")
     ap.add_argument("--timesteps", type=int, default=0)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--mode", default="rows", choices=["rows", "replicas"])
@@ -103,6 +103,21 @@ def measured_peaks():
         with open(path) as f:
             return json.load(f), "measured"
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def measured_traffic(mode, prec):
+    """DRAM bytes per launch of the forward / adjoint pair kernel from the committed `ncu --set full` capture
+    (profiles/*_traffic.json, written by scripts/summarize_profiles.py); None when no capture is committed."""
+    import glob
+
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json"))):
+        with open(path) as f:
+            doc = json.load(f)
+        for name, val in doc.get("kernels", {}).items():
+            if f",{mode}," in name and name.startswith("pair_kernel<" + ("float" if prec == "f32" else "double")):
+                best = {"bytes_per_launch": val, "source": doc.get("source")}
+    return best
 
 
 def ffma_peak_lanes():
@@ -325,7 +340,9 @@ def b200_arm(args):
             "frac": adj_rate / peak_slots,
             "peak_source": f"148 SM x {lanes} lanes x sm_max_mhz {sm_mhz:.0f} MHz ({peaks_src} MEASURED_PEAKS.json)",
             "algorithmic_slots_per_pair": a_slots, "pairs_per_launch": pairs_per_launch,
-            "avg_launch_ms": adj_ms, "traffic": None,
+            "avg_launch_ms": adj_ms,
+            "traffic": (measured_traffic("adj", prec) or {}).get("bytes_per_launch") if n == 20000 and T == 10 else None,
+            "traffic_source": (measured_traffic("adj", prec) or {}).get("source"),
             "forward_kernel": {"avg_launch_ms": fwd_ms, "achieved": fwd_rate / 1e12, "frac": fwd_rate / peak_slots,
                                "algorithmic_slots_per_pair": f_slots},
             "gradient": {"achieved": grad_rate / 1e12, "frac": grad_rate / peak_slots,

@@ -7,6 +7,9 @@ import sys
 
 so = "paper_1907_04839_b200/liblmshoot_b200.so"
 pat = sys.argv[1]
+for a in sys.argv[2:]:
+    if a.endswith((".so", ".cubin")):
+        so = a
 out = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
 blocks = out.split("Function : ")
 for b in blocks[1:]:

@@ -95,3 +95,19 @@ with open(f"profiles/{tag}_ncu_full.md", "w") as f:
         if k in ix:
             f.write(f"| `{k}` | {units[ix[k]]} | " + " | ".join(d[ix[k]] for d in data) + " |\n")
 print(open(f"profiles/{tag}_ncu_full.md").read()[:3000])
+
+# ---- DRAM traffic per launch of the dominant kernels (bench.py's roofline.traffic) ----------------------------------
+def kb(v, u):
+    return float(v) * {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1.0)
+
+
+traffic = {}
+for d in data:
+    name = short(d[ix["Kernel Name"]])
+    rd_b = kb(d[ix["dram__bytes_read.sum"]], units[ix["dram__bytes_read.sum"]])
+    wr_b = kb(d[ix["dram__bytes_write.sum"]], units[ix["dram__bytes_write.sum"]])
+    traffic.setdefault(name, []).append(rd_b + wr_b)
+out = {"source": f"profiles/{tag}_ncu_full.md (dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full)",
+       "kernels": {k: sum(v) / len(v) for k, v in traffic.items()}}
+json.dump(out, open(f"profiles/{tag}_traffic.json", "w"), indent=1)
+print(out)

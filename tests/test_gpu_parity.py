@@ -467,3 +467,34 @@ def test_nccl_path_single_rank(hs, monkeypatch, prec):
     assert got[0] == want[0] and np.array_equal(got[1], want[1])
     assert np.array_equal(s.final_q(), plain.final_q())
     s.close()
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_device_gaussian_kernel_values(hs, prec):
+    """gaussian_kernel known answers and the accuracy of the device exp over its whole range,
+    read back through velocities_at_step with one landmark of unit momentum: v = K(|x - q|^2) * (1, 0, 0)."""
+    s = hs(1, 3, prec)
+    q, p = np.zeros((1, 3)), np.array([[1.0, 0.0, 0.0]])
+    r = np.concatenate([[0.0, np.sqrt(2 * SIGMA**2 * np.log(2.0)), 1.5], np.linspace(0.0, 60.0, 4001)])
+    pts = np.zeros((r.size, 3))
+    pts[:, 1] = r
+    k = s.velocities_at_step(q, p, pts)[:, 0]
+    t = np.float32 if prec == "f32" else np.float64
+    r2 = (pts.astype(t)[:, 1] ** 2).astype(np.float64)
+    want = np.exp(r2 * (-0.5 / SIGMA**2))
+    assert k[0] == 1.0
+    assert k[1] == pytest.approx(0.5, rel=4e-7 if prec == "f32" else 1e-15)
+    assert k[2] == pytest.approx(0.606531, abs=5e-7)
+    # relative accuracy where K is normal; exact zero (flush) once exp underflows
+    if prec == "f64":
+        live = want > 1e-300
+        assert np.abs(k[live] / want[live] - 1).max() < 5e-13  # |arg| up to 690: the rounded scale costs ~|arg| ulp
+        near = want > 1e-12
+        assert np.abs(k[near] / want[near] - 1).max() < 2e-14
+        assert (k[want < 1e-320] == 0).all()
+    else:
+        live = want > 1e-30
+        assert np.abs(k[live] / want[live] - 1).max() < 2e-5
+        near = want > 1e-6
+        assert np.abs(k[near] / want[near] - 1).max() < 2e-6
+    assert (np.diff(k[3:]) <= 0).all()  # monotone in distance
