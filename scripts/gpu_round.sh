@@ -8,4 +8,8 @@ timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_default.log
 timeout 300 python bench.py --steps 10 --warmup 3 --variant 1 --no-extras > gpurun_out/bench_scalar.log 2>&1
 timeout 300 python bench.py --steps 5 --warmup 3 --precision f64 --no-extras > gpurun_out/bench_f64.log 2>&1
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.log 2>&1
-bash scripts/gpu_ncu.sh 0
+bash scripts/gpu_ncu.sh v0 --variant 0
+bash scripts/gpu_ncu.sh f64 --precision f64
+timeout 300 python bench.py --batch 128 --steps 5 --warmup 3 > gpurun_out/bench_batch.log 2>&1
+timeout 300 python bench.py --batch 128 --steps 5 --warmup 3 --precision f64 > gpurun_out/bench_batch_f64.log 2>&1
+timeout 1200 python scripts/sweep.py > gpurun_out/sweep.log 2>&1

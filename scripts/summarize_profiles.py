@@ -1,5 +1,5 @@
 """Turns gpurun_out/ ncu artefacts into the tracked summaries under profiles/ (run here, no GPU needed).
-usage: python scripts/summarize_profiles.py <tag> [variant]"""
+usage: python scripts/summarize_profiles.py <profiles-tag> [gpurun_out-tag] [bench args as text]"""
 import csv
 import io
 import json
@@ -10,11 +10,12 @@ import sys
 from collections import OrderedDict, defaultdict
 
 tag = sys.argv[1]
-variant = sys.argv[2] if len(sys.argv) > 2 else "0"
+variant = sys.argv[2] if len(sys.argv) > 2 else "v0"
+bench_args = sys.argv[3] if len(sys.argv) > 3 else ""
 os.makedirs("profiles", exist_ok=True)
 
 # ---- launch list: per-kernel share of the step ----------------------------------------------------------
-src = f"gpurun_out/launches_v{variant}.csv"
+src = f"gpurun_out/launches_{variant}.csv"
 rows = []
 with open(src) as f:
     lines = [l for l in f if not l.startswith("==")]
@@ -51,7 +52,7 @@ for _, n, v, _ in step:
     a[1] += v * scale
 shutil.copy(src, f"profiles/{tag}_launches.csv")
 with open(f"profiles/{tag}_launches.md", "w") as f:
-    f.write(f"# {tag}: ncu launch list of `python bench.py --steps 2 --warmup 3 --no-extras --variant {variant}`\n\n")
+    f.write(f"# {tag}: ncu launch list of `python bench.py --steps 2 --warmup 3 --no-extras {bench_args}`\n\n")
     f.write("`ncu --metrics gpu__time_duration.sum --clock-control none -c 400` (cold-cache, serialised: compare SHARES).\n")
     f.write(f"Raw list: `profiles/{tag}_launches.csv`.  One objective evaluation (launches {rows[prev][0]}..{rows[last-1][0]}):\n\n")
     f.write("| kernel | launches | total us | avg us | share of step |\n|---|---:|---:|---:|---:|\n")
@@ -61,7 +62,7 @@ with open(f"profiles/{tag}_launches.md", "w") as f:
 print(open(f"profiles/{tag}_launches.md").read())
 
 # ---- full capture: the counters the roofline discussion uses ---------------------------------------------------
-rep = f"gpurun_out/prof_v{variant}.ncu-rep"
+rep = f"gpurun_out/prof_{variant}.ncu-rep"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rd = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rd[0], rd[1], rd[2:]
@@ -87,8 +88,8 @@ keep = [
 ]
 with open(f"profiles/{tag}_ncu_full.md", "w") as f:
     f.write(f"# {tag}: `ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 38 -c 4` "
-            f"on `python bench.py --steps 1 --warmup 3 --no-extras --variant {variant}`\n\n")
-    f.write("Two forward and two adjoint pair-kernel launches of a warm-up evaluation (N = 20 000, T = 10, fp32).\n\n")
+            f"on `python bench.py --steps 1 --warmup 3 --no-extras {bench_args}`\n\n")
+    f.write("Two forward and two adjoint pair-kernel launches of a warm-up evaluation (N = 20 000, T = 10).\n\n")
     f.write("| metric | unit | " + " | ".join(short(d[ix["Kernel Name"]]) for d in data) + " |\n")
     f.write("|---|---|" + "---:|" * len(data) + "\n")
     for k in keep:
