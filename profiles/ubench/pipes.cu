@@ -195,6 +195,27 @@ __global__ void __launch_bounds__(256) pipe_kernel(float* out, long long* cycles
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) r += acc[k].x + acc[k].y;
+  } else if constexpr (MODE == 16) {  // 8 FFMA + 8 FADD per iteration: do FADD and FFMA share one pipe?
+    float acc[8], add[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { acc[k] = threadIdx.x * 1e-3f + k; add[k] = threadIdx.x * 2e-3f - k; }
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { acc[k] = fmaf(acc[k], a, b); add[k] = __fadd_rn(add[k], a); }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r += acc[k] + add[k];
+  } else if constexpr (MODE == 17) {  // 4 FFMA2 + 4 FADD2 per iteration
+    float2 acc[4], add[4];
+    float2 a2 = make_float2(a, a), b2 = make_float2(b, b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { acc[k] = make_float2(threadIdx.x * 1e-3f + k, k); add[k] = make_float2(threadIdx.x * 2e-3f - k, k); }
+    for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { acc[k] = __ffma2_rn(acc[k], a2, b2); add[k] = __fadd2_rn(add[k], a2); }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r += acc[k].x + acc[k].y + add[k].x + add[k].y;
   } else if constexpr (MODE == 13) {  // FMUL2 then dependent FFMA2 chain of length 3 x 8 independent (latency probe)
     float2 acc[2], x[2];
 #pragma unroll
@@ -312,6 +333,8 @@ int main(int argc, char** argv)
   run("ffma_3src", [&] { pipe_kernel<8><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 20, 1);
   run("ffma2_dep_chain_ilp2", [&] { pipe_kernel<13><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 8, 2);
   run("ffma_dep_chain_ilp2", [&] { pipe_kernel<14><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 16, 1);
+  run("mix_8ffma_8fadd", [&] { pipe_kernel<16><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 16, 1);
+  run("mix_4ffma2_4fadd2", [&] { pipe_kernel<17><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f); }, 8, 2);
   run("dfma", [&] { pipe_kernel_f64<0><<<grid, 256>>>(d_out64, d_cyc, 1.0001, 0.5); }, 8, 1);
   run("dadd", [&] { pipe_kernel_f64<1><<<grid, 256>>>(d_out64, d_cyc, 1.0001, 0.5); }, 8, 1);
   run("dmul", [&] { pipe_kernel_f64<2><<<grid, 256>>>(d_out64, d_cyc, 1.0001, 0.5); }, 8, 1);

@@ -105,3 +105,18 @@ def test_batch_handle_rejects_single_problem_calls():
         _lib.check(rc, br.handle)
     assert br.lib.lms_batch_size(br.handle) == 3
     br.close()
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_batched_two_dimensional(oracle, prec):
+    from paper_1907_04839_b200 import BatchedRegistrations
+
+    batch, n, T, lam = 4, 310, 6, 25.0
+    q0, p0, target = make_batch(batch, n, 33, dim=2)
+    br = BatchedRegistrations(SIGMA, n, batch, 2, prec, max_timesteps=T)
+    br.bind(q0, target, lam, T)
+    scalars, grad, div = br.evaluate(p0)
+    for b in range(batch):
+        loss, kin, mm, g = oracle.compute_gradient(prec, q0[b], p0[b], target[b], SIGMA, lam, T)
+        assert scalars[b, 0] == pytest.approx(loss, rel=TOL[prec]) and rel_inf(grad[b], g) <= TOL[prec]
+    br.close()

@@ -498,3 +498,52 @@ def test_device_gaussian_kernel_values(hs, prec):
         near = want > 1e-6
         assert np.abs(k[near] / want[near] - 1).max() < 2e-6
     assert (np.diff(k[3:]) <= 0).all()  # monotone in distance
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("sigma,spread,lam,T", [(0.1, 2.0, 10.0, 5), (100.0, 5.0, 10.0, 5), (1.5, 1e4, 1.0, 3),
+                                               (1.5, 0.0, 10.0, 4), (3.0, 4.0, 0.0, 1), (1.5, 6.0, 5e5, 40)])
+def test_parameter_extremes(oracle, prec, sigma, spread, lam, T):
+    """Kernel widths from 'no pair interacts' to 'every pair has K = 1', landmarks 1e4 mm apart (exp underflows for
+    almost every pair), coincident landmarks (spread 0: r = 0 for i != j), lambda = 0, T = 1 and the reference's
+    default T = 40."""
+    from paper_1907_04839_b200 import HamiltonianSystem
+
+    n = 300
+    rng = np.random.default_rng(int(sigma * 10) + T)
+    q = rng.uniform(-spread, spread, (n, 3)) if spread > 0 else np.zeros((n, 3))
+    p = 0.05 * rng.normal(size=(n, 3)) if sigma > 10 or spread == 0 else 0.75 * rng.normal(size=(n, 3))
+    target = q + 0.5 * rng.normal(size=(n, 3))
+    s = HamiltonianSystem(sigma, n, 3, prec, max_timesteps=T)
+    r = s.compute_gradient(q, p, target, lam, T)
+    loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, sigma, lam, T)
+    tol = TOL[prec] * (10 if prec == "f32" and (sigma > 10 or spread == 0) else 1)  # N coherent terms per row in fp32
+    assert r.loss == pytest.approx(loss, rel=tol) and r.kinetic == pytest.approx(kin, rel=tol, abs=1e-300)
+    assert r.mismatch == pytest.approx(mm, rel=tol)
+    assert rel_inf(r.grad, grad) <= tol
+    s.close()
+
+
+def test_large_n_row_subset_fp32(oracle):
+    """N = 200 000 (BASELINE configs[2] size on one GPU): 48 rows of one forward and one adjoint launch against the
+    oracle's identical per-row sums; run-to-run bitwise determinism at that size."""
+    from paper_1907_04839_b200 import HamiltonianSystem, make_template_points, rng_normals
+
+    n = 200000
+    q = make_template_points(n, 40.0 * float(np.sqrt(n / 1847.0)))
+    p = (0.75 * rng_normals(3, n * 3)).reshape(n, 3)
+    alpha = rng_normals(4, n * 3).reshape(n, 3)
+    beta = rng_normals(5, n * 3).reshape(n, 3)
+    rows = np.unique(np.concatenate([[0, 511, 512, n - 1], np.random.default_rng(1).integers(0, n, 44)]))
+    s = HamiltonianSystem(SIGMA, n, 3, "f32", max_timesteps=1)
+    hq, hp = s.derivatives(q, p)
+    ohq, ohp = oracle.pair_rows("f32", q, p, rows, SIGMA)
+    assert np.abs(hq[rows] - ohq).max() <= 1e-5 * np.abs(hq).max()
+    assert np.abs(hp[rows] - ohp).max() <= 1e-5 * np.abs(hp).max()
+    da, db = s.adjoint_step(q, p, alpha, beta)
+    oda, odb = oracle.pair_rows("f32", q, p, rows, SIGMA, alpha, beta)
+    assert np.abs(da[rows] - oda).max() <= 1e-5 * np.abs(da).max()
+    assert np.abs(db[rows] - odb).max() <= 1e-5 * np.abs(db).max()
+    again = s.derivatives(q, p)
+    assert np.array_equal(again[0], hq) and np.array_equal(again[1], hp)
+    s.close()
