@@ -395,7 +395,6 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
   const long long G = gridDim.x;
   long long c = cells * blockIdx.x / G;
   const long long c_end = cells * (blockIdx.x + 1) / G;
-  const long long first_rt_local = c / nJ;  // first row tile (local index) this CTA touches
 
   while (c < c_end) {
     const long long rt_local = c / nJ;
@@ -551,7 +550,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     const long long cta_last = ((cell_hi + 1) * G - 1) / cells;
     bool do_epilogue = true;
     if (cta_first != cta_last) {
-      const long long slot = (long long)blockIdx.x * a.max_seg + (rt_local - first_rt_local);
+      // slot of segment `ord` of row tile rt_local: rt_local * max_seg + ord (ord = CTA index - first CTA)
+      const long long slot = rt_local * a.max_seg + ((long long)blockIdx.x - cta_first);
       T* mine = a.partials + slot * (NA * BM);
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -559,8 +559,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         for (int k = 0; k < NA; ++k) __stcg(mine + k * BM + r * kThreads + tid, acc[r][k]);
       __threadfence();
       __syncthreads();
+      const int nseg = (int)(cta_last - cta_first + 1);
       if (tid == 0) {
-        const int nseg = (int)(cta_last - cta_first + 1);
         const int prev = atomicAdd(a.counters + rt_local, 1);
         const int last = prev == nseg - 1;
         if (last) a.counters[rt_local] = 0;  // everyone has arrived: re-arm for the next launch
@@ -574,10 +574,11 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         for (int r = 0; r < R; ++r)
 #pragma unroll
           for (int k = 0; k < NA; ++k) acc[r][k] = T(0);
-        for (long long cta = cta_first; cta <= cta_last; ++cta) {
-          const long long cb = cells * cta / G;
-          const long long s = cta * a.max_seg + (rt_local - cb / nJ);
-          const T* theirs = a.partials + s * (NA * BM);
+        // ascending segment order = ascending columns; loads of several segments are in flight together
+        const T* seg0 = a.partials + rt_local * a.max_seg * (long long)(NA * BM);
+#pragma unroll 4
+        for (int ord = 0; ord < nseg; ++ord) {
+          const T* theirs = seg0 + (long long)ord * (NA * BM);
 #pragma unroll
           for (int r = 0; r < R; ++r)
 #pragma unroll

@@ -253,10 +253,14 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   // going finer -- 32 columns per CTA -- makes N = 1000..2000 slower, 0.30 -> 0.43 ms and 0.35 -> 0.88 ms per
   // gradient: the partial-slot write / fence / counter / re-read chain costs more than the extra parallelism.)
   p.grid = (int)std::min<long long>(full, std::max<long long>(cells / kUnitsPerTile, 1));
-  const long long per_cta = (cells + p.grid - 1) / p.grid;
-  p.max_seg = (int)((per_cta + units_per_row - 1) / units_per_row) + 1;
+  // mid-size problems: a whole number of CTAs per SM, so no SM carries one CTA more than its neighbours
+  if (p.grid < full && p.grid > num_sms_) p.grid -= p.grid % num_sms_;
+  // partial slots are indexed (row tile, segment): a row tile is shared by at most max_seg CTAs, since every
+  // CTA owns at least floor(cells / grid) consecutive units
+  const long long per_cta_min = std::max<long long>(cells / p.grid, 1);
+  p.max_seg = (int)((units_per_row + per_cta_min - 1) / per_cta_min) + 1;
   constexpr int NA = Shape<MODE, D>::kAcc;
-  p.partial_elems = (size_t)p.grid * p.max_seg * NA * p.bm;
+  p.partial_elems = (size_t)p.n_row_tiles * p.max_seg * NA * p.bm;
   return p;
 }
 
