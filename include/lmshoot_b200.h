@@ -209,6 +209,15 @@ int lms_row_partition(size_t n, int world, int rank, long long* slice, long long
                       long long* row_end);
 int lms_system_comm_init(lms_system* sys, const unsigned char id[128], int rank, int world);
 
+/* Loopback transport for the same row partition: `world` ranks are handles in ONE process (one host thread
+ * each, typically on one GPU); the per-step exchange is a rendezvous plus device-to-device copies instead of
+ * NCCL.  Same schedule, same slice layout; it lets a single-GPU machine run the partitioned evaluation with
+ * world > 1.  Every rank must call lms_objective_eval concurrently from its own thread. */
+typedef struct lms_local_group lms_local_group;
+int lms_local_group_create(int world, lms_local_group** out);
+void lms_local_group_destroy(lms_local_group* group);
+int lms_system_join_local_group(lms_system* sys, lms_local_group* group, int rank);
+
 /* ---- synthetic inputs (synth.hpp:15-43, rng.hpp) ---- */
 
 /* Rng(seed).normal() / uniform() streams (rng.hpp:19-41; std::mt19937_64). */

@@ -8,12 +8,12 @@ from .errors import CommError, CudaError, DivergedError, NumericalError, ShapeEr
 from .lbfgs import LbfgsParams, MinimizeResult, minimize  # noqa: F401
 from .registration import RegistrationResult, register_landmarks  # noqa: F401
 from .shooting import (GradientResult, HamiltonianSystem, ShootingConfig, comm_unique_id, gaussian_kernel,  # noqa: F401
-                       kernel_scale, row_partition)
+                       kernel_scale, row_partition, LocalGroup)
 from .synth import make_synthetic_pair, make_template_points, rng_normals, rng_uniforms  # noqa: F401
 
 __all__ = [
     "HamiltonianSystem", "BatchedRegistrations", "BatchRegistrationResult", "ShootingConfig", "GradientResult", "LbfgsParams", "MinimizeResult", "minimize",
     "register_landmarks", "RegistrationResult", "make_synthetic_pair", "make_template_points", "rng_normals",
-    "rng_uniforms", "gaussian_kernel", "kernel_scale", "comm_unique_id", "row_partition", "ShapeError", "DivergedError",
+    "rng_uniforms", "gaussian_kernel", "kernel_scale", "comm_unique_id", "row_partition", "LocalGroup", "ShapeError", "DivergedError",
     "NumericalError", "CudaError", "StateError", "CommError",
 ]

@@ -268,6 +268,30 @@ int lms_comm_unique_id(unsigned char id[128])
   return LMS_OK;
 }
 
+struct lms_local_group {
+  lms::LocalGroup* impl;
+};
+
+int lms_local_group_create(int world, lms_local_group** out)
+{
+  if (!out || world < 1 || world > 64) return LMS_ERR_INVALID;
+  *out = new (std::nothrow) lms_local_group{new (std::nothrow) lms::LocalGroup(world)};
+  return *out && (*out)->impl ? LMS_OK : LMS_ERR_CUDA;
+}
+
+void lms_local_group_destroy(lms_local_group* group)
+{
+  if (!group) return;
+  delete group->impl;
+  delete group;
+}
+
+int lms_system_join_local_group(lms_system* sys, lms_local_group* group, int rank)
+{
+  if (!group) return LMS_ERR_INVALID;
+  return guarded(sys, [&](lms::SystemBase* s) { s->join_local_group(group->impl, rank); });
+}
+
 int lms_row_partition(size_t n, int world, int rank, long long* slice, long long* stride, long long* row_begin,
                       long long* row_end)
 {

@@ -13,7 +13,7 @@ typedef struct {
   char internal[128];
 } ncclUniqueId;
 typedef int ncclResult_t;  // ncclSuccess == 0
-enum : int { kNcclFloat32 = 7, kNcclFloat64 = 8 };
+enum : int { kNcclInt8 = 0, kNcclFloat32 = 7, kNcclFloat64 = 8 };
 
 struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;

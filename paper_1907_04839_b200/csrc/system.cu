@@ -660,10 +660,7 @@ void System<T, D>::enqueue_eval(bool timed, int count, const int* d_ids)
   }
   if (comm_active_) {
     // every rank ends with the full gradient (row-major double rows are contiguous per rank slice)
-    const NcclApi& nc = nccl_api();
-    const size_t slice = (size_t)(stride_ / world_) * D;
-    if (nc.AllGather(d_grad_ + rank_ * slice, d_grad_, slice, kNcclFloat64, comm_, stream_) != 0)
-      throw StatusError{LMS_ERR_COMM, "ncclAllGather(grad) failed"};
+    gather_inplace({{reinterpret_cast<char*>(d_grad_), (size_t)(stride_ / world_) * D * sizeof(double)}});
   }
   final_adj_ = cur;
 }
@@ -903,21 +900,15 @@ void System<T, D>::warp_stored(size_t m, const double* pts, double* out)
   sync();
 }
 
-// ---- row partition over NCCL ------------------------------------------------------------------------------------------
+// ---- row partition: NCCL over NVLink, or the in-process loopback group -------------------------------------------
+// Re-lay the planes so that every rank owns an equal, tile-aligned slice (in-place all-gather).
 template <typename T, int D>
-void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
+void System<T, D>::relayout_for_world(int world, int rank)
 {
-  if (world < 1 || rank < 0 || rank >= world) throw StatusError{LMS_ERR_INVALID, "bad rank/world"};
-  // world == 1 normally needs no communicator; LMS_FORCE_NCCL=1 keeps the NCCL path on so that a single-GPU
-  // box can exercise it (tests/test_gpu_parity.py::test_nccl_path_single_rank).
-  const char* force = std::getenv("LMS_FORCE_NCCL");
-  if (world == 1 && !(force && force[0] == '1')) return;
-  const NcclApi& nc = nccl_api();
-  if (!nc.ok) throw StatusError{LMS_ERR_COMM, "libnccl.so.2 could not be loaded"};
+  if (batch != 1) throw StatusError{LMS_ERR_STATE, "batches are not row-partitioned"};
   sync();
   destroy_graph();
   bound = false;
-  // Re-lay the planes so that every rank owns an equal, tile-aligned slice (in-place all-gather).
   const long long new_stride = partition_rows((long long)cfg.n, world, rank).stride;
   if (new_stride != stride_) {
     stride_ = new_stride;
@@ -925,6 +916,9 @@ void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
     dev_free(traj_); dev_free(adj_[0]); dev_free(adj_[1]); dev_free(hp0_); dev_free(target_); dev_free(q0_);
     dev_free(scratch_in_); dev_free(scratch_out_); dev_free(d_x_); dev_free(d_grad_); dev_free(h_part_);
     dev_free(mm_part_);
+    bs_traj_ = (long long)(max_t_ + 1) * kState * stride_;
+    bs_state_ = (long long)kState * stride_;
+    bs_vec_ = (long long)D * stride_;
     traj_ = dev_alloc_zero<T>((size_t)(max_t_ + 1) * kState * plane);
     adj_[0] = dev_alloc_zero<T>(kState * plane);
     adj_[1] = dev_alloc_zero<T>(kState * plane);
@@ -939,12 +933,76 @@ void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
     h_part_ = dev_alloc_zero<double>(part_tiles_);
     mm_part_ = dev_alloc_zero<double>(part_tiles_);
   }
+  rank_ = rank;
+  world_ = world;
+}
+
+template <typename T, int D>
+void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
+{
+  if (world < 1 || rank < 0 || rank >= world) throw StatusError{LMS_ERR_INVALID, "bad rank/world"};
+  // world == 1 normally needs no communicator; LMS_FORCE_NCCL=1 keeps the NCCL path on so that a single-GPU
+  // box can exercise it (tests/test_gpu_parity.py::test_nccl_path_single_rank).
+  const char* force = std::getenv("LMS_FORCE_NCCL");
+  if (world == 1 && !(force && force[0] == '1')) return;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) throw StatusError{LMS_ERR_COMM, "libnccl.so.2 could not be loaded"};
+  relayout_for_world(world, rank);
   ncclUniqueId uid;
   std::memcpy(uid.internal, id, sizeof(uid.internal));
   if (nc.CommInitRank(&comm_, world, uid, rank) != 0) throw StatusError{LMS_ERR_COMM, "ncclCommInitRank failed"};
-  rank_ = rank;
-  world_ = world;
+  local_ = nullptr;
   comm_active_ = true;
+}
+
+template <typename T, int D>
+void System<T, D>::join_local_group(LocalGroup* group, int rank)
+{
+  if (!group || rank < 0 || rank >= group->world) throw StatusError{LMS_ERR_INVALID, "bad rank/world"};
+  relayout_for_world(group->world, rank);
+  local_ = group;
+  comm_active_ = true;
+}
+
+// The one exchange primitive: every buffer is `world` slices of `bytes`; rank r's slice r is final on this rank
+// and the other slices are filled from the peers.
+template <typename T, int D>
+void System<T, D>::gather_inplace(const std::vector<std::pair<char*, size_t>>& buffers)
+{
+  if (local_ == nullptr) {
+    const NcclApi& nc = nccl_api();
+    bool ok = nc.GroupStart() == 0;
+    for (const auto& b : buffers)
+      ok = ok && nc.AllGather(b.first + rank_ * b.second, b.first, b.second, kNcclInt8, comm_, stream_) == 0;
+    ok = (nc.GroupEnd() == 0) && ok;
+    if (!ok) throw StatusError{LMS_ERR_COMM, "ncclAllGather failed"};
+    return;
+  }
+  // loopback: my slices are final once my stream drains; publish, meet, pull the peers' slices, meet again so
+  // that nobody overwrites a buffer a peer is still reading
+  cudaError_t e = cudaStreamSynchronize(stream_);
+  {
+    std::lock_guard<std::mutex> lock(local_->m);
+    local_->lists[rank_] = buffers;
+    if (e != cudaSuccess) local_->failed = true;
+  }
+  local_->barrier();
+  if (!local_->failed) {
+    for (int p = 0; p < world_ && e == cudaSuccess; ++p) {
+      if (p == rank_) continue;
+      const auto& theirs = local_->lists[p];
+      for (size_t k = 0; k < buffers.size() && k < theirs.size() && e == cudaSuccess; ++k)
+        e = cudaMemcpyAsync(buffers[k].first + p * buffers[k].second, theirs[k].first + p * theirs[k].second,
+                            buffers[k].second, cudaMemcpyDeviceToDevice, stream_);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream_);
+    if (e != cudaSuccess) {
+      std::lock_guard<std::mutex> lock(local_->m);
+      local_->failed = true;
+    }
+  }
+  local_->barrier();
+  if (local_->failed) throw StatusError{LMS_ERR_COMM, "loopback exchange failed"};
 }
 
 // In-place all-gather of every plane of a (q,p) or (alpha,beta) state: rank r contributes rows
@@ -952,26 +1010,18 @@ void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
 template <typename T, int D>
 void System<T, D>::all_gather_state(T* planes)
 {
-  const NcclApi& nc = nccl_api();
-  const size_t slice = (size_t)(stride_ / world_);
-  const int dtype = sizeof(T) == 4 ? kNcclFloat32 : kNcclFloat64;
-  bool ok = nc.GroupStart() == 0;
-  for (int k = 0; k < kState && ok; ++k) {
-    T* plane = planes + (long long)k * stride_;
-    ok = nc.AllGather(plane + rank_ * slice, plane, slice, dtype, comm_, stream_) == 0;
-  }
-  ok = (nc.GroupEnd() == 0) && ok;
-  if (!ok) throw StatusError{LMS_ERR_COMM, "ncclAllGather(state) failed"};
+  const size_t slice_bytes = (size_t)(stride_ / world_) * sizeof(T);
+  std::vector<std::pair<char*, size_t>> buffers;
+  for (int k = 0; k < kState; ++k)
+    buffers.emplace_back(reinterpret_cast<char*>(planes + (long long)k * stride_), slice_bytes);
+  gather_inplace(buffers);
 }
 
 // Per-row-tile double partials: tiles are indexed globally, each rank filled its own contiguous range.
 template <typename T, int D>
 void System<T, D>::all_gather_doubles(double* buf)
 {
-  const NcclApi& nc = nccl_api();
-  const size_t slice = (size_t)(part_tiles_ / world_);
-  if (nc.AllGather(buf + rank_ * slice, buf, slice, kNcclFloat64, comm_, stream_) != 0)
-    throw StatusError{LMS_ERR_COMM, "ncclAllGather(partials) failed"};
+  gather_inplace({{reinterpret_cast<char*>(buf), (size_t)(part_tiles_ / world_) * sizeof(double)}});
 }
 
 RowPartition partition_rows(long long n, int world, int rank)

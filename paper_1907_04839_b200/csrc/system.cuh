@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -39,6 +41,34 @@ struct StatusError {
 constexpr unsigned long long kNotDiverged = ~0ull;
 constexpr int kRowAlign = 512;  // planes are padded to a multiple of the largest row tile
 
+// Loopback transport for the row partition: `world` ranks are handles in ONE process (one host thread each,
+// typically all on the same GPU).  Same schedule and the same in-place slice layout as the NCCL path; the
+// exchange is a rendezvous plus device-to-device copies.  It exists so that a single-GPU box can run the
+// partitioned evaluation with world > 1 for real (tests/test_gpu_parity.py::test_row_partition_loopback).
+struct LocalGroup {
+  explicit LocalGroup(int w) : world(w), lists(w) {}
+  int world;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long generation = 0;
+  std::vector<std::vector<std::pair<char*, size_t>>> lists;  // per rank: (buffer base, slice bytes)
+  bool failed = false;
+
+  void barrier()
+  {
+    std::unique_lock<std::mutex> lock(m);
+    const unsigned long long gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lock, [&] { return generation != gen; });
+    }
+  }
+};
+
 // Abstract interface the C ABI talks to (one concrete System<T,D> per precision x dim).
 class SystemBase {
  public:
@@ -55,6 +85,7 @@ class SystemBase {
   virtual void velocities(const double* q, const double* p, size_t m, const double* pts, double* out) = 0;
   virtual void warp_stored(size_t m, const double* pts, double* out) = 0;
   virtual void comm_init(const unsigned char* id, int rank, int world) = 0;
+  virtual void join_local_group(LocalGroup* group, int rank) = 0;
   // population batches: `count` problems listed in ids (all when ids == nullptr); arrays are full-batch sized
   virtual void eval_batch(const double* x, double* grad, double* scalars, int* diverged_step, int count,
                           const int* ids) = 0;
@@ -126,6 +157,7 @@ class System final : public SystemBase {
   void velocities(const double* q, const double* p, size_t m, const double* pts, double* out) override;
   void warp_stored(size_t m, const double* pts, double* out) override;
   void comm_init(const unsigned char* id, int rank, int world) override;
+  void join_local_group(LocalGroup* group, int rank) override;
   void eval_batch(const double* x, double* grad, double* scalars, int* diverged_step, int count,
                   const int* ids) override;
   void final_q_batch(double* out) override;
@@ -156,6 +188,8 @@ class System final : public SystemBase {
   void ensure_points(size_t m);
   void all_gather_state(T* state_planes);
   void all_gather_doubles(double* buf);
+  void gather_inplace(const std::vector<std::pair<char*, size_t>>& buffers);
+  void relayout_for_world(int world, int rank);
 
   cudaStream_t stream_ = nullptr;
   int num_sms_ = 0;
@@ -211,6 +245,7 @@ class System final : public SystemBase {
   int rank_ = 0, world_ = 1;
   bool comm_active_ = false;
   ncclComm_t comm_ = nullptr;
+  LocalGroup* local_ = nullptr;
   int row_tile_begin_(int bm) const;
   int row_tile_end_(int bm) const;
 };

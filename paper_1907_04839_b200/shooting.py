@@ -239,6 +239,10 @@ class HamiltonianSystem:
         return out
 
     # -- multi-GPU row partition ------------------------------------------------------------------------------------------
+    def join_local_group(self, group, rank: int):
+        """Row partition over the in-process loopback transport (see LocalGroup)."""
+        self._check(self.lib.lms_system_join_local_group(self.handle, group.handle, rank))
+
     def comm_init(self, unique_id: bytes, rank: int, world: int):
         buf = (ctypes.c_ubyte * 128).from_buffer_copy(unique_id)
         self._check(self.lib.lms_system_comm_init(self.handle, buf, rank, world))
@@ -272,3 +276,19 @@ def row_partition(n, world, rank):
     vals = [c_longlong() for _ in range(4)]
     _lib.check(lib.lms_row_partition(n, world, rank, *[ctypes.byref(v) for v in vals]))
     return tuple(v.value for v in vals)
+
+
+class LocalGroup:
+    """`world` ranks as handles in one process (lms_local_group_*): the row partition's loopback transport."""
+
+    def __init__(self, world):
+        self.lib = _lib.load()
+        self.world = int(world)
+        handle = c_void_p()
+        _lib.check(self.lib.lms_local_group_create(self.world, ctypes.byref(handle)))
+        self.handle = handle
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.lms_local_group_destroy(self.handle)
+            self.handle = None

@@ -547,3 +547,56 @@ def test_large_n_row_subset_fp32(oracle):
     again = s.derivatives(q, p)
     assert np.array_equal(again[0], hq) and np.array_equal(again[1], hp)
     s.close()
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("world,n", [(2, 1500), (3, 2600), (4, 700), (2, 20000)])
+def test_row_partition_loopback(hs, oracle, prec, world, n):
+    """The row-partitioned evaluation with world > 1 on ONE GPU: every rank is a handle driven by its own host
+    thread, the per-step exchange goes through the loopback transport (same schedule and slice layout as the
+    NCCL path).  Every rank must end with the same full gradient, equal to the unpartitioned result."""
+    import threading
+
+    from paper_1907_04839_b200 import HamiltonianSystem, LocalGroup
+
+    T, lam = 5, 100.0
+    q, p, target, *_ = synth_case(n, 3, 500 + n + world, spread=10.0 if n < 10000 else 60.0)
+    plain = hs(n, 3, prec)
+    plain.bind_registration(q, target, lam, T)
+    want_loss, want_grad = plain.objective(p)
+    want_q = plain.final_q()
+    group = LocalGroup(world)
+    ranks = [HamiltonianSystem(SIGMA, n, 3, prec, max_timesteps=T) for _ in range(world)]
+    results, errors = [None] * world, []
+
+    def run(r):
+        try:
+            s = ranks[r]
+            s.join_local_group(group, r)
+            s.bind_registration(q, target, lam, T)
+            first = s.objective(p)
+            second = s.objective(p)  # a second evaluation reuses the buffers the first one exchanged through
+            results[r] = (first, second, s.last_kinetic, s.last_mismatch, s.final_q())
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    tol = 1e-12 if prec == "f64" else 2e-6
+    for r in range(world):
+        (loss, grad), (loss2, grad2), kin, mm, fq = results[r]
+        assert loss == results[0][0][0] and np.array_equal(grad, results[0][0][1])  # identical on every rank
+        assert loss2 == loss and np.array_equal(grad2, grad)                          # and run to run
+        assert loss == pytest.approx(want_loss, rel=tol) and rel_inf(grad, want_grad) <= tol
+        assert kin == pytest.approx(plain.last_kinetic, rel=tol) and mm == pytest.approx(plain.last_mismatch, rel=tol)
+        assert rel_inf(fq, want_q) <= tol
+    if n <= 3000:
+        o = oracle.compute_gradient(prec, q, p, target, SIGMA, lam, T)
+        assert rel_inf(results[0][0][1], o[3]) <= TOL[prec]
+    for s in ranks:
+        s.close()
+    group.close()
