@@ -596,7 +596,7 @@ def test_row_partition_loopback(hs, oracle, prec, world, n):
         assert rel_inf(fq, want_q) <= tol
     if n <= 3000:
         o = oracle.compute_gradient(prec, q, p, target, SIGMA, lam, T)
-        assert rel_inf(results[0][0][1], o[3]) <= TOL[prec]
+        assert rel_inf(results[0][0][1].reshape(n, 3), o[3]) <= TOL[prec]
     for s in ranks:
         s.close()
     group.close()
