@@ -368,7 +368,7 @@ __device__ __forceinline__ double block_sum(double v, double* scratch)
 // ---------------------------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------------------------
-template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false>
+template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1>
 __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> a)
 {
   static_assert(!PACKED || (sizeof(T) == 4 && R % 2 == 0), "the packed path is fp32 with an even row count");
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       }
       const int jj_lo = col0 > jt * kTileJ ? col0 - jt * kTileJ : 0;
       const int jj_hi = col1 < (jt + 1) * kTileJ ? col1 - jt * kTileJ : kTileJ;
-#pragma unroll 1
+#pragma unroll UNR
       for (int jj = jj_lo; jj < jj_hi; jj += JU) {
         T cj[JU][NC];
 #pragma unroll

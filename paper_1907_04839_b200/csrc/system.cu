@@ -35,17 +35,18 @@ void dev_free(T*& p)
 #define LMS_PICK2(D, MODE, R, JU, MINB, NAME) make_choice<float, D, MODE, R, JU, MINB, true>(NAME)
 
 // fp32, D = 3.  Variant 0 (default) is the packed f32x2 pair the B200 sessions in profiles/ measured fastest:
-// 64-register forward kernel (8 CTAs/SM) and 96-register adjoint kernel (5 CTAs/SM).  1 = the scalar-FFMA
-// kernels (first version, kept as the A/B baseline); 2-4 = other packed shapes.
+// forward R=2, 4 columns per LDS.128, 72 registers (7 CTAs/SM); adjoint R=2, 2 columns per load with the column
+// loop unrolled twice, 96 registers (5 CTAs/SM).  1 = the scalar-FFMA kernels (first version, kept as the A/B
+// baseline); 2 = the previous packed default; 3, 4 = other packed shapes.
 template <>
 KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
 {
   switch (v) {
     case 1: return LMS_PICK(float, 3, kFwd, 4, 4, 3, "fwd_f32_r4_j4");
-    case 2: return LMS_PICK2(3, kFwd, 4, 2, 4, "fwd_f32x2_r4_j2");
-    case 3: return LMS_PICK2(3, kFwd, 2, 2, 6, "fwd_f32x2_r2_j2_b6");
-    case 4: return LMS_PICK2(3, kFwd, 6, 1, 3, "fwd_f32x2_r6_j1");
-    default: return LMS_PICK2(3, kFwd, 2, 2, 8, "fwd_f32x2_r2_j2_b8");
+    case 2: return LMS_PICK2(3, kFwd, 2, 2, 8, "fwd_f32x2_r2_j2_b8");
+    case 3: return make_choice<float, 3, kFwd, 2, 1, 7, true, 4>("fwd_f32x2_r2_j1_b7_u4");
+    case 4: return LMS_PICK2(3, kFwd, 4, 2, 4, "fwd_f32x2_r4_j2");
+    default: return LMS_PICK2(3, kFwd, 2, 4, 7, "fwd_f32x2_r2_j4_b7");
   }
 }
 template <>
@@ -53,10 +54,10 @@ KernelChoice<float> pick_kernel<float, 3, kAdj>(int v)
 {
   switch (v) {
     case 1: return LMS_PICK(float, 3, kAdj, 2, 4, 3, "adj_f32_r2_j4");
-    case 2: return LMS_PICK2(3, kAdj, 2, 2, 4, "adj_f32x2_r2_j2_b4");
-    case 3: return LMS_PICK2(3, kAdj, 2, 1, 6, "adj_f32x2_r2_j1_b6");
+    case 2: return LMS_PICK2(3, kAdj, 2, 2, 5, "adj_f32x2_r2_j2_b5");
+    case 3: return make_choice<float, 3, kAdj, 2, 1, 4, true, 2>("adj_f32x2_r2_j1_b4_u2");
     case 4: return LMS_PICK2(3, kAdj, 4, 1, 3, "adj_f32x2_r4_j1");
-    default: return LMS_PICK2(3, kAdj, 2, 2, 5, "adj_f32x2_r2_j2_b5");
+    default: return make_choice<float, 3, kAdj, 2, 2, 5, true, 2>("adj_f32x2_r2_j2_b5_u2");
   }
 }
 template <>
@@ -91,12 +92,12 @@ KernelChoice<double> pick_kernel<double, 3, kVel>(int)
 template <>
 KernelChoice<float> pick_kernel<float, 2, kFwd>(int)
 {
-  return LMS_PICK2(2, kFwd, 2, 2, 8, "fwd_f32x2_d2_r2_j2");
+  return LMS_PICK2(2, kFwd, 2, 4, 7, "fwd_f32x2_d2_r2_j4");
 }
 template <>
 KernelChoice<float> pick_kernel<float, 2, kAdj>(int)
 {
-  return LMS_PICK2(2, kAdj, 2, 2, 5, "adj_f32x2_d2_r2_j2");
+  return make_choice<float, 2, kAdj, 2, 2, 5, true, 2>("adj_f32x2_d2_r2_j2_u2");
 }
 template <>
 KernelChoice<float> pick_kernel<float, 2, kVel>(int)
