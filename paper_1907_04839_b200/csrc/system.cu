@@ -72,7 +72,8 @@ KernelChoice<double> pick_kernel<double, 3, kFwd>(int v)
   switch (v) {
     case 1: return LMS_PICK(double, 3, kFwd, 1, 2, 4, "fwd_f64_r1_j2");
     case 2: return LMS_PICK(double, 3, kFwd, 4, 2, 2, "fwd_f64_r4_j2");
-    default: return LMS_PICK(double, 3, kFwd, 2, 2, 3, "fwd_f64_r2_j2");
+    case 3: return LMS_PICK(double, 3, kFwd, 2, 2, 3, "fwd_f64_r2_j2");
+    default: return make_choice<double, 3, kFwd, 2, 2, 3, false, 2>("fwd_f64_r2_j2_u2");
   }
 }
 template <>
@@ -81,7 +82,8 @@ KernelChoice<double> pick_kernel<double, 3, kAdj>(int v)
   switch (v) {
     case 1: return LMS_PICK(double, 3, kAdj, 1, 2, 3, "adj_f64_r1_j2");
     case 2: return LMS_PICK(double, 3, kAdj, 2, 1, 2, "adj_f64_r2_j1");
-    default: return LMS_PICK(double, 3, kAdj, 2, 2, 2, "adj_f64_r2_j2");
+    case 3: return LMS_PICK(double, 3, kAdj, 2, 2, 2, "adj_f64_r2_j2");
+    default: return make_choice<double, 3, kAdj, 2, 2, 2, false, 2>("adj_f64_r2_j2_u2");
   }
 }
 template <>
