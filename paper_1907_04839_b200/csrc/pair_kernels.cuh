@@ -313,6 +313,44 @@ __device__ __forceinline__ long long row_of(int rt, int r, int tid)
     return (long long)rt * (kThreads * R) + r * kThreads + tid;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Bulk-async (TMA) staging of column tiles: one elected thread issues cp.async.bulk copies of the
+// contiguous 128-column chunk of every component plane straight into shared memory; completion is
+// tracked by an mbarrier (complete_tx), so no thread spends registers or LDG/STS slots on staging.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count)
+{
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes)
+{
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar)
+{
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity)
+{
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LMS_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra LMS_DONE_%=;\n"
+      "bra LMS_WAIT_%=;\n"
+      "LMS_DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // Vector load of JU consecutive columns of one staged component.
 template <typename T, int JU>
 struct ColVec;
@@ -368,7 +406,7 @@ __device__ __forceinline__ double block_sum(double v, double* scratch)
 // ---------------------------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------------------------
-template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1>
+template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false>
 __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> a)
 {
   static_assert(!PACKED || (sizeof(T) == 4 && R % 2 == 0), "the packed path is fp32 with an even row count");
@@ -382,6 +420,17 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
   __shared__ double red_scratch[kThreads];
   __shared__ double exp_tbl[16];  // fp64 only: 2^(j/16) for Math<double>::kernel
   __shared__ int s_last;
+  __shared__ __align__(8) unsigned long long tile_bar[2];  // BULK only: one mbarrier per tile buffer
+  int buf = 0;                // tile buffer in use; kept across row tiles so the mbarrier phases stay in step
+  unsigned wait_parity = 0;   // bit b: parity the next wait on buffer b must observe
+  if constexpr (BULK) {
+    if (threadIdx.x == 0) {
+      mbar_init(&tile_bar[0], 1);
+      mbar_init(&tile_bar[1], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
   if constexpr (sizeof(T) == 8) {
     if (threadIdx.x < 16) exp_tbl[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
@@ -452,13 +501,23 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 
     // ---- sweep the j tiles [jt0, jt1) with register-prefetched double buffering ---------------
     // (only columns [col0, col1) of the first and last tile are accumulated)
-    T stage[NC];
+    T stage[BULK ? 1 : NC];
+    auto issue_tile = [&](int jt, int b) {  // BULK: called by thread 0 only
+      mbar_expect_tx(&tile_bar[b], (unsigned)(NC * kTileJ * sizeof(T)));
 #pragma unroll
-    for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)jt0 * kTileJ + tid];
-    int buf = 0;
+      for (int k = 0; k < NC; ++k)
+        bulk_g2s(&tile[b][k][0], col_plane(k) + (long long)jt * kTileJ, (unsigned)(kTileJ * sizeof(T)), &tile_bar[b]);
+    };
+    if constexpr (BULK) {
+      if (tid == 0) issue_tile(jt0, buf);  // buffer `buf` was last read before the previous __syncthreads
+    } else {
 #pragma unroll
-    for (int k = 0; k < NC; ++k) tile[0][k][tid] = stage[k];
-    __syncthreads();
+      for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)jt0 * kTileJ + tid];
+      buf = 0;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) tile[0][k][tid] = stage[k];
+      __syncthreads();
+    }
 
     // packed path only: two rows per 64-bit register pair; -q_i (or -x_i) first, the rest as they are
     constexpr int RP = PACKED ? R / 2 : 1;
@@ -483,9 +542,15 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 
     for (int jt = jt0; jt < jt1; ++jt) {
       const bool more = jt + 1 < jt1;
-      if (more) {
+      if constexpr (BULK) {
+        if (more && tid == 0) issue_tile(jt + 1, buf ^ 1);
+        mbar_wait(&tile_bar[buf], (wait_parity >> buf) & 1u);
+        wait_parity ^= 1u << buf;
+      } else {
+        if (more) {
 #pragma unroll
-        for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)(jt + 1) * kTileJ + tid];
+          for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)(jt + 1) * kTileJ + tid];
+        }
       }
       const int jj_lo = col0 > jt * kTileJ ? col0 - jt * kTileJ : 0;
       const int jj_hi = col1 < (jt + 1) * kTileJ ? col1 - jt * kTileJ : kTileJ;
@@ -517,9 +582,11 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
           }
         }
       }
-      if (more) {
+      if constexpr (!BULK) {
+        if (more) {
 #pragma unroll
-        for (int k = 0; k < NC; ++k) tile[buf ^ 1][k][tid] = stage[k];
+          for (int k = 0; k < NC; ++k) tile[buf ^ 1][k][tid] = stage[k];
+        }
       }
       __syncthreads();
       buf ^= 1;

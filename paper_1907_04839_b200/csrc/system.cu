@@ -37,7 +37,9 @@ void dev_free(T*& p)
 // fp32, D = 3.  Variant 0 (default) is the packed f32x2 pair the B200 sessions in profiles/ measured fastest:
 // forward R=2, 4 columns per LDS.128, 72 registers (7 CTAs/SM); adjoint R=2, 2 columns per load with the column
 // loop unrolled twice, 96 registers (5 CTAs/SM).  1 = the scalar-FFMA kernels (first version, kept as the A/B
-// baseline); 2 = the previous packed default; 3, 4 = other packed shapes.
+// baseline); 2 = the previous packed default; 3, 4 = other packed shapes; 5 = the default shapes with the column
+// tiles staged by bulk-async copies (TMA, cp.async.bulk + mbarrier) instead of register-staged loads -- measured
+// 1 % slower in fp32 (8.21 vs 8.10 ms) and 1 % faster in fp64, where it is the default.
 template <>
 KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
 {
@@ -46,6 +48,7 @@ KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
     case 2: return LMS_PICK2(3, kFwd, 2, 2, 8, "fwd_f32x2_r2_j2_b8");
     case 3: return make_choice<float, 3, kFwd, 2, 1, 7, true, 4>("fwd_f32x2_r2_j1_b7_u4");
     case 4: return LMS_PICK2(3, kFwd, 4, 2, 4, "fwd_f32x2_r4_j2");
+    case 5: return make_choice<float, 3, kFwd, 2, 4, 7, true, 1, true>("fwd_f32x2_r2_j4_b7_tma");
     default: return LMS_PICK2(3, kFwd, 2, 4, 7, "fwd_f32x2_r2_j4_b7");
   }
 }
@@ -57,6 +60,7 @@ KernelChoice<float> pick_kernel<float, 3, kAdj>(int v)
     case 2: return LMS_PICK2(3, kAdj, 2, 2, 5, "adj_f32x2_r2_j2_b5");
     case 3: return make_choice<float, 3, kAdj, 2, 1, 4, true, 2>("adj_f32x2_r2_j1_b4_u2");
     case 4: return LMS_PICK2(3, kAdj, 4, 1, 3, "adj_f32x2_r4_j1");
+    case 5: return make_choice<float, 3, kAdj, 2, 2, 5, true, 2, true>("adj_f32x2_r2_j2_b5_u2_tma");
     default: return make_choice<float, 3, kAdj, 2, 2, 5, true, 2>("adj_f32x2_r2_j2_b5_u2");
   }
 }
@@ -73,7 +77,8 @@ KernelChoice<double> pick_kernel<double, 3, kFwd>(int v)
     case 1: return LMS_PICK(double, 3, kFwd, 1, 2, 4, "fwd_f64_r1_j2");
     case 2: return LMS_PICK(double, 3, kFwd, 4, 2, 2, "fwd_f64_r4_j2");
     case 3: return LMS_PICK(double, 3, kFwd, 2, 2, 3, "fwd_f64_r2_j2");
-    default: return make_choice<double, 3, kFwd, 2, 2, 3, false, 2>("fwd_f64_r2_j2_u2");
+    case 5: return make_choice<double, 3, kFwd, 2, 2, 3, false, 2>("fwd_f64_r2_j2_u2");
+    default: return make_choice<double, 3, kFwd, 2, 2, 3, false, 2, true>("fwd_f64_r2_j2_u2_tma");
   }
 }
 template <>
@@ -83,7 +88,8 @@ KernelChoice<double> pick_kernel<double, 3, kAdj>(int v)
     case 1: return LMS_PICK(double, 3, kAdj, 1, 2, 3, "adj_f64_r1_j2");
     case 2: return LMS_PICK(double, 3, kAdj, 2, 1, 2, "adj_f64_r2_j1");
     case 3: return LMS_PICK(double, 3, kAdj, 2, 2, 2, "adj_f64_r2_j2");
-    default: return make_choice<double, 3, kAdj, 2, 2, 2, false, 2>("adj_f64_r2_j2_u2");
+    case 5: return make_choice<double, 3, kAdj, 2, 2, 2, false, 2>("adj_f64_r2_j2_u2");
+    default: return make_choice<double, 3, kAdj, 2, 2, 2, false, 2, true>("adj_f64_r2_j2_u2_tma");
   }
 }
 template <>

@@ -115,11 +115,11 @@ struct KernelChoice {
   const char* name = "";
 };
 
-template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1>
+template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false>
 KernelChoice<T> make_choice(const char* name)
 {
   KernelChoice<T> c;
-  c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR>;
+  c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK>;
   c.rows_per_thread = R;
   c.name = name;
   return c;

@@ -122,7 +122,7 @@ def test_two_dimensional_landmarks(hs, oracle, prec):
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-@pytest.mark.parametrize("variant", [1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
 def test_kernel_variants_agree_with_oracle(hs, oracle, prec, variant):
     tol = TOL[prec]
     n = 700
