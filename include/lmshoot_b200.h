@@ -170,6 +170,14 @@ int lms_minimize(lms_objective_fn fn, void* user, size_t n, const double* x0,
 int lms_register(lms_system* sys, const lms_lbfgs_params* params, double* momenta_out,
                  double* warped_out, lms_minimize_result* result, double* hist_loss);
 
+/* The same registration with the optimiser's vectors resident in HBM: x, g, d, the trial
+ * point and the curvature pairs never leave the device, dot products come back as one double each, and the
+ * objective runs through lms_objective_eval_device.  Same decision logic as lms_minimize / lbfgs.cpp:186-282;
+ * sums are deterministic but not in the reference's sequential order, so iterates agree with lms_register to
+ * rounding, not bit for bit. */
+int lms_register_device(lms_system* sys, const lms_lbfgs_params* params, double* momenta_out,
+                        double* warped_out, lms_minimize_result* result, double* hist_loss);
+
 /* ---- population batches (BASELINE configs[3]; no counterpart in the single-problem reference) ---- */
 
 /* A handle that holds `batch` independent registrations of cfg->n landmarks each (same sigma, dim,

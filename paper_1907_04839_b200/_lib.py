@@ -95,6 +95,7 @@ SIGNATURES = {
     "lms_batch_final_q": ([c_void_p, _dp], c_int),
     "lms_batch_register": ([c_void_p, POINTER(LmsLbfgsParams), _dp, _dp, POINTER(LmsMinimizeResult), POINTER(c_int),
                             POINTER(c_int)], c_int),
+    "lms_register_device": ([c_void_p, POINTER(LmsLbfgsParams), _dp, _dp, POINTER(LmsMinimizeResult), _dp], c_int),
     "lms_comm_unique_id": ([POINTER(c_ubyte)], c_int),
     "lms_row_partition": ([c_size_t, c_int, c_int, POINTER(c_longlong), POINTER(c_longlong), POINTER(c_longlong),
                            POINTER(c_longlong)], c_int),

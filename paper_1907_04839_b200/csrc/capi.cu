@@ -10,7 +10,7 @@
 
 #include "system.cuh"
 
-struct lms_system {
+struct lms_system {  // layout shared with device_lbfgs.cu
   lms::SystemBase* impl = nullptr;
   int device = 0;
 };

@@ -90,6 +90,7 @@ class SystemBase {
   virtual void eval_batch(const double* x, double* grad, double* scalars, int* diverged_step, int count,
                           const int* ids) = 0;
   virtual void final_q_batch(double* out) = 0;
+  virtual cudaStream_t stream_handle() const = 0;
   int batch = 1;
 
   lms_config cfg{};
@@ -161,6 +162,7 @@ class System final : public SystemBase {
   void eval_batch(const double* x, double* grad, double* scalars, int* diverged_step, int count,
                   const int* ids) override;
   void final_q_batch(double* out) override;
+  cudaStream_t stream_handle() const override { return stream_; }
 
  private:
   static constexpr int kState = 2 * D;  // planes per (q,p) or (alpha,beta) state

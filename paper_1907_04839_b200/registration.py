@@ -43,9 +43,11 @@ def max_dist(a, b):
 
 
 def register_landmarks(template, target, config: ShootingConfig | None = None, grad_tol=1e-6, device=0,
-                       system: HamiltonianSystem | None = None) -> RegistrationResult:
+                       system: HamiltonianSystem | None = None, device_vectors=False,
+                       already_bound=False) -> RegistrationResult:
     """register_landmarks (registration.hpp:48-50) without Procrustes: runs wholly through the C ABI
-    (lms_register): device objective + the library's host L-BFGS driver."""
+    (lms_register): device objective + the library's host L-BFGS driver; ``device_vectors=True`` keeps the
+    optimiser's vectors in HBM as well (lms_register_device)."""
     config = config or ShootingConfig()
     config.validate()
     template = np.ascontiguousarray(np.asarray(template, dtype=np.float64))
@@ -60,14 +62,16 @@ def register_landmarks(template, target, config: ShootingConfig | None = None, g
         system = HamiltonianSystem(config.sigma, n, dim, config.precision, device=device,
                                    max_timesteps=config.timesteps)
     try:
-        system.bind_registration(template, target, config.lam, config.timesteps)
+        if not already_bound:  # binding uploads q0/target and captures the evaluation graph (a few ms)
+            system.bind_registration(template, target, config.lam, config.timesteps)
         lib = system.lib
         params = LbfgsParams(max_iter=config.max_iter, grad_tol=grad_tol).to_c()
         dp = POINTER(c_double)
         momenta, warped = np.empty((n, dim)), np.empty((n, dim))
         hist = np.zeros(config.max_iter)
         res = _lib.LmsMinimizeResult()
-        _lib.check(lib.lms_register(system.handle, ctypes.byref(params), momenta.ctypes.data_as(dp),
+        entry = lib.lms_register_device if device_vectors else lib.lms_register
+        _lib.check(entry(system.handle, ctypes.byref(params), momenta.ctypes.data_as(dp),
                                     warped.ctypes.data_as(dp), ctypes.byref(res), hist.ctypes.data_as(dp)),
                    system.handle)
     finally:

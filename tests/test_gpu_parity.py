@@ -600,3 +600,34 @@ def test_row_partition_loopback(hs, oracle, prec, world, n):
     for s in ranks:
         s.close()
     group.close()
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_device_resident_lbfgs_matches_host_driver(prec):
+    """lms_register_device (optimiser vectors in HBM) against lms_register (host vectors,
+    the reference's summation order): same decision logic, sums differ by rounding only."""
+    from paper_1907_04839_b200 import DivergedError, ShootingConfig, register_landmarks
+
+    n, T, lam, iters = 1500, 8, 1e4, 30
+    rng = np.random.default_rng(31)
+    q0 = rng.uniform(-15, 15, (n, 3))
+    target = q0 + 0.5 * rng.normal(size=(n, 3))
+    cfg = ShootingConfig(sigma=SIGMA, timesteps=T, lam=lam, max_iter=iters, precision=prec)
+    host = register_landmarks(q0, target, cfg)
+    dev = register_landmarks(q0, target, cfg, device_vectors=True)
+    assert dev.initial_loss == host.initial_loss
+    assert dev.reason == host.reason
+    if prec == "f64":
+        assert (dev.iterations, dev.evaluations) == (host.iterations, host.evaluations)
+        assert dev.final_loss == pytest.approx(host.final_loss, rel=1e-8)
+        assert np.abs(dev.warped - host.warped).max() <= 1e-6
+        assert np.allclose(dev.hist_loss, host.hist_loss, rtol=1e-8)
+    else:
+        assert dev.final_loss == pytest.approx(host.final_loss, rel=0.05)
+        assert np.abs(dev.warped - host.warped).max() <= 5e-3
+    assert dev.final_loss < 0.5 * dev.initial_loss
+    bad = q0.copy()
+    bad[5, 0] = np.nan
+    with pytest.raises(DivergedError) as e:
+        register_landmarks(bad, target, cfg, device_vectors=True)
+    assert e.value.timestep == 0
