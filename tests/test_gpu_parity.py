@@ -631,3 +631,18 @@ def test_device_resident_lbfgs_matches_host_driver(prec):
     with pytest.raises(DivergedError) as e:
         register_landmarks(bad, target, cfg, device_vectors=True)
     assert e.value.timestep == 0
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_full_size_full_gradient_vs_cpu_oracle(hs, oracle, full_case, prec):
+    """N = 20 000 (BASELINE configs[1]), every row: the complete objective evaluation against the CPU oracle on
+    all host threads.  T = 2 keeps the oracle's (2T+2) N^2 passes to a few seconds."""
+    n, _, q0, target, p_true, x0 = full_case
+    T, lam = 2, 5e5
+    s = hs(n, 3, prec, max_t=10)
+    r = s.compute_gradient(q0, x0 * 5.0, target, lam, T)  # x0 was built for T = 10: rescale to land near the target
+    loss, kin, mm, grad = oracle.compute_gradient(prec, q0, x0 * 5.0, target, SIGMA, lam, T)
+    assert r.loss == pytest.approx(loss, rel=TOL[prec])
+    assert r.kinetic == pytest.approx(kin, rel=TOL[prec])
+    assert r.mismatch == pytest.approx(mm, rel=TOL[prec])
+    assert rel_inf(r.grad, grad) <= TOL[prec]
