@@ -45,7 +45,7 @@ def parse_args():
     ap.add_argument("--mode", default="rows", choices=["rows", "replicas"])
     ap.add_argument("--batch", type=int, default=0, help="population mode: B registrations of --n landmarks per GPU")
     ap.add_argument("--no-extras", action="store_true", help="skip fp64, L-BFGS and cpu_baseline legs")
-    ap.add_argument("--lbfgs-iters", type=int, default=10)
+    ap.add_argument("--lbfgs-iters", type=int, default=30)
     return ap.parse_args()
 
 

@@ -8,7 +8,12 @@
 // strictly sequential order, so iterates agree with the host driver to rounding, not bit for bit.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "lbfgs_core.hpp"
@@ -75,10 +80,13 @@ __global__ void __launch_bounds__(kRedThreads) reduce3_kernel(const double* __re
   }
 }
 
-// The whole two-loop recursion in ONE launch (single CTA, so the 2m dependent dot products need no host round
-// trip): d = -H g, out[0] = g.d.  Dots: per-thread strided partial + fixed shared-memory tree (deterministic).
+// The whole two-loop recursion in ONE cooperative launch over all SMs: d = -H g, out[0] = g.d.  Every thread owns
+// a fixed grid-stride set of elements for the whole kernel, so the axpy after a dot needs no barrier; a dot is
+// per-CTA tree -> one partial per CTA -> grid barrier -> every CTA adds the partials in ascending CTA order
+// (deterministic, the same value everywhere).  2m + 1 grid barriers replace 2m + 1 single-SM passes over memory
+// (measured at N = 20 000, m = 10: ~0.7 ms -> ~0.1 ms per iteration).
 constexpr int kMaxPairs = 32;
-constexpr int kLoopThreads = 1024;
+constexpr int kLoopThreads = 256;
 struct PairSet {
   const double* s[kMaxPairs];
   const double* y[kMaxPairs];
@@ -86,13 +94,90 @@ struct PairSet {
   int m;
 };
 
-__device__ double block_dot(const double* a, const double* b, size_t n, double* scratch)
+// Grid barrier on a monotonically increasing counter (the launch is cooperative, so every CTA is resident).
+__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch)
 {
-  double t = 0.0;
-  for (size_t i = threadIdx.x; i < n; i += kLoopThreads) t = fma(a[i], b[i], t);
-  scratch[threadIdx.x] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    epoch += gridDim.x;
+    __threadfence();
+    atomicAdd(counter, 1u);
+    while (*reinterpret_cast<volatile unsigned*>(counter) < epoch) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Sum over the grid of one double per thread; `slot` selects a fresh partial array per call (no reuse hazards).
+__device__ double grid_sum(double v, double* scratch, double* partials, int slot, unsigned* counter, unsigned& epoch)
+{
+  scratch[threadIdx.x] = v;
   __syncthreads();
   for (int h = kLoopThreads / 2; h >= 1; h >>= 1) {
+    if (threadIdx.x < h) scratch[threadIdx.x] += scratch[threadIdx.x + h];
+    __syncthreads();
+  }
+  double* mine = partials + (size_t)slot * gridDim.x;
+  if (threadIdx.x == 0) __stcg(mine + blockIdx.x, scratch[0]);
+  grid_barrier(counter, epoch);
+  // every CTA adds the gridDim.x <= kLoopThreads partials with the same fixed tree: one parallel load, 8 steps
+  scratch[threadIdx.x] = threadIdx.x < gridDim.x ? __ldcg(mine + threadIdx.x) : 0.0;
+  __syncthreads();
+  for (int h = kLoopThreads / 2; h >= 1; h >>= 1) {
+    if (threadIdx.x < h) scratch[threadIdx.x] += scratch[threadIdx.x + h];
+    __syncthreads();
+  }
+  const double t = scratch[0];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(kLoopThreads) two_loop_kernel(PairSet ps, double gamma, const double* __restrict__ g,
+                                                                double* __restrict__ d, size_t n,
+                                                                double* __restrict__ partials, unsigned* counter,
+                                                                double* __restrict__ out)
+{
+  __shared__ double scratch[kLoopThreads];
+  __shared__ double coef[kMaxPairs];
+  unsigned epoch = 0;  // the host zeroes the counter before every launch
+  const size_t first = (size_t)blockIdx.x * kLoopThreads + threadIdx.x;
+  const size_t step = (size_t)gridDim.x * kLoopThreads;
+  for (size_t i = first; i < n; i += step) d[i] = g[i];
+  int slot = 0;
+  for (int k = ps.m - 1; k >= 0; --k) {
+    double t = 0.0;
+    for (size_t i = first; i < n; i += step) t = fma(ps.s[k][i], d[i], t);
+    const double a = ps.rho[k] * grid_sum(t, scratch, partials, slot++, counter, epoch);
+    if (threadIdx.x == 0) coef[k] = a;
+    for (size_t i = first; i < n; i += step) d[i] = fma(-a, ps.y[k][i], d[i]);
+  }
+  for (size_t i = first; i < n; i += step) d[i] *= gamma;
+  __syncthreads();
+  for (int k = 0; k < ps.m; ++k) {
+    double t = 0.0;
+    for (size_t i = first; i < n; i += step) t = fma(ps.y[k][i], d[i], t);
+    const double b = ps.rho[k] * grid_sum(t, scratch, partials, slot++, counter, epoch);
+    const double c = coef[k] - b;
+    for (size_t i = first; i < n; i += step) d[i] = fma(c, ps.s[k][i], d[i]);
+  }
+  double t = 0.0;
+  for (size_t i = first; i < n; i += step) {
+    const double di = -d[i];
+    d[i] = di;
+    t = fma(g[i], di, t);
+  }
+  const double slope = grid_sum(t, scratch, partials, slot++, counter, epoch);
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = slope;
+}
+
+__device__ double block_dot(const double* a, const double* b, size_t n, double* scratch, int threads)
+{
+  double t = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += threads) t = fma(a[i], b[i], t);
+  scratch[threadIdx.x] = t;
+  __syncthreads();
+  for (int h = threads / 2; h >= 1; h >>= 1) {
     if (threadIdx.x < h) scratch[threadIdx.x] += scratch[threadIdx.x + h];
     __syncthreads();
   }
@@ -101,43 +186,16 @@ __device__ double block_dot(const double* a, const double* b, size_t n, double* 
   return r;
 }
 
-__global__ void __launch_bounds__(kLoopThreads) two_loop_kernel(PairSet ps, double gamma, const double* __restrict__ g,
-                                                                double* __restrict__ d, size_t n,
-                                                                double* __restrict__ out)
-{
-  __shared__ double scratch[kLoopThreads];
-  __shared__ double coef[kMaxPairs];
-  for (size_t i = threadIdx.x; i < n; i += kLoopThreads) d[i] = g[i];
-  __syncthreads();
-  for (int k = ps.m - 1; k >= 0; --k) {
-    const double a = ps.rho[k] * block_dot(ps.s[k], d, n, scratch);
-    if (threadIdx.x == 0) coef[k] = a;
-    for (size_t i = threadIdx.x; i < n; i += kLoopThreads) d[i] = fma(-a, ps.y[k][i], d[i]);
-    __syncthreads();
-  }
-  for (size_t i = threadIdx.x; i < n; i += kLoopThreads) d[i] *= gamma;
-  __syncthreads();
-  for (int k = 0; k < ps.m; ++k) {
-    const double b = ps.rho[k] * block_dot(ps.y[k], d, n, scratch);
-    const double c = coef[k] - b;
-    for (size_t i = threadIdx.x; i < n; i += kLoopThreads) d[i] = fma(c, ps.s[k][i], d[i]);
-    __syncthreads();
-  }
-  for (size_t i = threadIdx.x; i < n; i += kLoopThreads) d[i] = -d[i];
-  __syncthreads();
-  const double slope = block_dot(g, d, n, scratch);
-  if (threadIdx.x == 0) out[0] = slope;
-}
-
 // out[0..2] = s.y, s.s, y.y in one launch (single CTA)
-__global__ void __launch_bounds__(kLoopThreads) pair_stats_kernel(const double* __restrict__ s,
+constexpr int kStatThreads = 1024;
+__global__ void __launch_bounds__(kStatThreads) pair_stats_kernel(const double* __restrict__ s,
                                                                   const double* __restrict__ y, size_t n,
                                                                   double* __restrict__ out)
 {
-  __shared__ double scratch[kLoopThreads];
-  const double sy = block_dot(s, y, n, scratch);
-  const double ss = block_dot(s, s, n, scratch);
-  const double yy = block_dot(y, y, n, scratch);
+  __shared__ double scratch[kStatThreads];
+  const double sy = block_dot(s, y, n, scratch, kStatThreads);
+  const double ss = block_dot(s, s, n, scratch, kStatThreads);
+  const double yy = block_dot(y, y, n, scratch, kStatThreads);
   if (threadIdx.x == 0) {
     out[0] = sy;
     out[1] = ss;
@@ -167,6 +225,29 @@ __global__ void take_step_kernel(double* __restrict__ s, double* __restrict__ y,
   }
 }
 
+// Device scratch of the driver, allocated once per handle (SystemBase::lbfgs_workspace) and reused by every
+// lms_register_device call with the same vector length and memory.
+struct Workspace {
+  size_t n = 0, count = 0, each = 0;
+  double* slab = nullptr;           // `count` vectors of `each` doubles
+  double* loop_partials = nullptr;  // two-loop kernel: (2 kMaxPairs + 1) x loop_blocks
+  unsigned* loop_counter = nullptr;
+  int loop_blocks = 1;
+  double* partials = nullptr;       // reduce3_kernel
+  unsigned* counter = nullptr;
+  double* h_out = nullptr;          // mapped pinned: 3 doubles
+  double* d_out = nullptr;          // its device alias
+  ~Workspace()
+  {
+    if (slab) cudaFree(slab);
+    if (loop_partials) cudaFree(loop_partials);
+    if (loop_counter) cudaFree(loop_counter);
+    if (partials) cudaFree(partials);
+    if (counter) cudaFree(counter);
+    if (h_out) cudaFreeHost(h_out);
+  }
+};
+
 struct DeviceOps {
   using Vec = double*;
   size_t n;
@@ -176,26 +257,59 @@ struct DeviceOps {
   unsigned* counter = nullptr;
   double* h_out = nullptr;  // mapped pinned: 3 doubles
   double* d_out = nullptr;  // its device alias
-  std::vector<Vec> pool;
+  std::vector<Vec> pool, extra;
+  double t_obj = 0, t_loop = 0, t_red = 0;  // wall-clock breakdown (LMS_TRACE)
+  int n_obj = 0, n_red = 0;
 
   void check(cudaError_t e)
   {
     if (e != cudaSuccess) throw lms::CudaFailure{e, "device_lbfgs", __LINE__};
   }
-  void init()
+  // One allocation for every vector the driver can hold at once (x, g, d, trial point and gradient, best
+  // gradient, 2 (memory + 1) curvature vectors), made on the first call and kept on the handle.
+  double* loop_partials = nullptr;
+  unsigned* loop_counter = nullptr;
+  int loop_blocks = 1;
+  void init(int memory)
   {
-    check(cudaMalloc(&partials, 3 * kRedBlocks * sizeof(double)));
-    check(cudaMalloc(&counter, sizeof(unsigned)));
-    check(cudaMemset(counter, 0, sizeof(unsigned)));
-    check(cudaHostAlloc(&h_out, 3 * sizeof(double), cudaHostAllocMapped));
-    check(cudaHostGetDevicePointer(&d_out, h_out, 0));
+    const size_t count = 2 * ((size_t)std::max(memory, 0) + 1) + 6;
+    auto ws = std::static_pointer_cast<Workspace>(sys->lbfgs_workspace);
+    if (!ws || ws->n != n || ws->count < count) {
+      sys->lbfgs_workspace.reset();
+      ws = std::make_shared<Workspace>();
+      ws->n = n;
+      ws->count = count;
+      ws->each = ((n ? n : 1) + 31) / 32 * 32;
+      check(cudaMalloc(&ws->slab, ws->count * ws->each * sizeof(double)));
+      // the two-loop kernel: one CTA per SM (cooperative launch: all resident), fewer when the vector is short
+      int dev = 0, sms = 0;
+      check(cudaGetDevice(&dev));
+      check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      ws->loop_blocks = (int)std::max<size_t>(
+          1, std::min<size_t>(std::min<size_t>((size_t)sms, kLoopThreads), (n + kLoopThreads - 1) / kLoopThreads));
+      check(cudaMalloc(&ws->loop_partials, (size_t)(2 * kMaxPairs + 1) * ws->loop_blocks * sizeof(double)));
+      check(cudaMalloc(&ws->loop_counter, sizeof(unsigned)));
+      check(cudaMalloc(&ws->partials, 3 * kRedBlocks * sizeof(double)));
+      check(cudaMalloc(&ws->counter, sizeof(unsigned)));
+      check(cudaMemset(ws->counter, 0, sizeof(unsigned)));
+      check(cudaHostAlloc(&ws->h_out, 3 * sizeof(double), cudaHostAllocMapped));
+      check(cudaHostGetDevicePointer(&ws->d_out, ws->h_out, 0));
+      sys->lbfgs_workspace = ws;
+    }
+    for (size_t k = 0; k < ws->count; ++k) pool.push_back(ws->slab + (ws->count - 1 - k) * ws->each);
+    loop_partials = ws->loop_partials;
+    loop_counter = ws->loop_counter;
+    loop_blocks = ws->loop_blocks;
+    partials = ws->partials;
+    counter = ws->counter;
+    h_out = ws->h_out;
+    d_out = ws->d_out;
+    // an aborted run (divergence) may have left the arrival counter of reduce3_kernel mid-count
+    check(cudaMemsetAsync(counter, 0, sizeof(unsigned), stream));
   }
   void destroy()
   {
-    for (Vec v : pool) cudaFree(v);
-    if (partials) cudaFree(partials);
-    if (counter) cudaFree(counter);
-    if (h_out) cudaFreeHost(h_out);
+    for (Vec v : extra) cudaFree(v);
   }
   int blocks() const { return (int)((n + 255) / 256); }
 
@@ -206,8 +320,9 @@ struct DeviceOps {
       pool.pop_back();
       return v;
     }
-    Vec v = nullptr;
+    Vec v = nullptr;  // beyond the slab (not reached by minimize_core's allocation pattern)
     check(cudaMalloc(&v, (n ? n : 1) * sizeof(double)));
+    extra.push_back(v);
     return v;
   }
   void release(Vec v) { pool.push_back(v); }
@@ -224,9 +339,12 @@ struct DeviceOps {
       return;
     }
     const int nb = (int)std::min<size_t>(kRedBlocks, (n + kRedThreads - 1) / kRedThreads);
+    const auto t0 = std::chrono::steady_clock::now();
     reduce3_kernel<<<nb, kRedThreads, 0, stream>>>(a, b, n, partials, counter, d_out);
     check(cudaGetLastError());
     check(cudaStreamSynchronize(stream));
+    t_red += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    ++n_red;
   }
   double dot(Vec a, Vec b)
   {
@@ -279,9 +397,14 @@ struct DeviceOps {
       ps.y[k] = hy[k];
       ps.rho[k] = rho[k];
     }
-    two_loop_kernel<<<1, kLoopThreads, 0, stream>>>(ps, gamma, g, d, n, d_out);
-    check(cudaGetLastError());
+    const auto t0 = std::chrono::steady_clock::now();
+    check(cudaMemsetAsync(loop_counter, 0, sizeof(unsigned), stream));
+    const double* gp = g;
+    void* args[] = {&ps, &gamma, &gp, &d, &n, &loop_partials, &loop_counter, &d_out};
+    check(cudaLaunchCooperativeKernel((const void*)two_loop_kernel, dim3(loop_blocks), dim3(kLoopThreads), args, 0,
+                                      stream));
     check(cudaStreamSynchronize(stream));
+    t_loop += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return h_out[0];
   }
   void pair_stats(Vec s, Vec y, double* sy, double* ss, double* yy)
@@ -290,7 +413,7 @@ struct DeviceOps {
       *sy = *ss = *yy = 0.0;
       return;
     }
-    pair_stats_kernel<<<1, kLoopThreads, 0, stream>>>(s, y, n, d_out);
+    pair_stats_kernel<<<1, kStatThreads, 0, stream>>>(s, y, n, d_out);
     check(cudaGetLastError());
     check(cudaStreamSynchronize(stream));
     *sy = h_out[0];
@@ -300,7 +423,10 @@ struct DeviceOps {
   double objective(Vec x, Vec grad)
   {
     double sc[3] = {0, 0, 0};
+    const auto t0 = std::chrono::steady_clock::now();
     sys->eval(x, grad, sc, true);  // throws lms::StatusError (e.g. LMS_ERR_DIVERGED) to abort, like DivergedError
+    t_obj += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    ++n_obj;
     return sc[0];
   }
 };
@@ -322,13 +448,24 @@ extern "C" int lms_register_device(lms_system* handle, const lms_lbfgs_params* p
   int rc = LMS_OK;
   try {
     if (cudaSetDevice(handle->device) != cudaSuccess) return LMS_ERR_CUDA;
-    ops.init();
+    const bool trace = std::getenv("LMS_TRACE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms_since = [&](std::chrono::steady_clock::time_point t) {
+      return std::chrono::duration<double, std::milli>(now() - t).count();
+    };
+    auto t_begin = now();
+    ops.init(params->memory);
+    if (trace) std::fprintf(stderr, "[lms] register_device: init %.3f ms\n", ms_since(t_begin));
     std::vector<double> x0(nd ? nd : 1);
     for (size_t e = 0; e < nd; ++e) x0[e] = (s->host_target[e] - s->host_q0[e]) / s->timesteps;  // registration.cpp:47-52
     double* x = ops.make();
     double* g = ops.make();
     ops.check(cudaMemcpyAsync(x, x0.data(), nd * sizeof(double), cudaMemcpyHostToDevice, ops.stream));
+    auto t_min = now();
     rc = lms::minimize_core(ops, x, g, *params, result, hist_loss, nullptr, nullptr, nullptr);
+    if (trace)
+      std::fprintf(stderr, "[lms] register_device: minimize %.3f ms (objective %.3f ms in %d calls, two-loop %.3f ms, "
+                   "reductions %.3f ms in %d)\n", ms_since(t_min), ops.t_obj, ops.n_obj, ops.t_loop, ops.t_red, ops.n_red);
     if (rc == LMS_OK) {
       ops.check(cudaMemcpyAsync(momenta_out, x, nd * sizeof(double), cudaMemcpyDeviceToHost, ops.stream));
       ops.check(cudaStreamSynchronize(ops.stream));
@@ -350,6 +487,12 @@ extern "C" int lms_register_device(lms_system* handle, const lms_lbfgs_params* p
   } catch (...) {
     rc = LMS_ERR_CUDA;
   }
-  ops.destroy();
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    ops.destroy();
+    if (std::getenv("LMS_TRACE"))
+      std::fprintf(stderr, "[lms] register_device: teardown %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
   return rc;
 }

@@ -406,21 +406,32 @@ __device__ __forceinline__ double block_sum(double v, double* scratch)
 // ---------------------------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------------------------
-template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false>
+// AOS: the shared-memory tile holds each column's NC components contiguously (column-major), filled by
+// the register-staged path (every thread transposes its own column with 16-byte stores), so one column
+// costs NC/4 LDS.128 with only NC registers of column data live (the plane layout needs JU = 4 columns,
+// 4 NC registers, for the same load count).
+template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false,
+          bool AOS = false>
 __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> a)
 {
   static_assert(!PACKED || (sizeof(T) == 4 && R % 2 == 0), "the packed path is fp32 with an even row count");
+  static_assert(!AOS || (sizeof(T) == 4 && JU == 1 && !BULK && Shape<MODE, D>::kColComps % 4 == 0),
+                "column-major tiles: fp32, one column per step, register-staged, 16-byte multiples");
   using S = Shape<MODE, D>;
   constexpr int NC = S::kColComps;
   constexpr int NR = S::kRowComps;
   constexpr int NA = S::kAcc;
   constexpr int BM = kThreads * R;
 
-  __shared__ __align__(16) T tile[2][NC][kTileJ];
+  __shared__ __align__(16) T tile[2][AOS ? kTileJ : NC][AOS ? NC : kTileJ];
   __shared__ double red_scratch[kThreads];
   __shared__ double exp_tbl[16];  // fp64 only: 2^(j/16) for Math<double>::kernel
   __shared__ int s_last;
   __shared__ __align__(8) unsigned long long tile_bar[2];  // BULK only: one mbarrier per tile buffer
+  // Programmatic dependent launch: the next launch of the evaluation may start scheduling its CTAs as soon as
+  // every CTA of this one is running, so they take over SM slots as ours retire and the launch latency
+  // between the 2T dependent steps disappears.  A no-op when the launch carries no PDL attribute.
+  asm volatile("griddepcontrol.launch_dependents;");
   int buf = 0;                // tile buffer in use; kept across row tiles so the mbarrier phases stay in step
   unsigned wait_parity = 0;   // bit b: parity the next wait on buffer b must observe
   if constexpr (BULK) {
@@ -435,6 +446,9 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     if (threadIdx.x < 16) exp_tbl[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
   }
+
+  // everything above touched no global memory; everything below reads what the previous launch wrote
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int tid = threadIdx.x;
   // Work is counted in units of kUnitJ columns of one row tile, so every CTA's share differs by at most
@@ -515,7 +529,10 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)jt0 * kTileJ + tid];
       buf = 0;
 #pragma unroll
-      for (int k = 0; k < NC; ++k) tile[0][k][tid] = stage[k];
+      for (int k = 0; k < NC; ++k) {
+        if constexpr (AOS) tile[0][tid][k] = stage[k];
+        else tile[0][k][tid] = stage[k];
+      }
       __syncthreads();
     }
 
@@ -557,12 +574,20 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 #pragma unroll UNR
       for (int jj = jj_lo; jj < jj_hi; jj += JU) {
         T cj[JU][NC];
+        if constexpr (AOS) {
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          T v[JU];
-          ColVec<T, JU>::load(&tile[buf][k][jj], v);
+          for (int k = 0; k < NC; k += 4) {
+            const float4 t4 = *reinterpret_cast<const float4*>(&tile[buf][jj][k]);
+            cj[0][k] = t4.x; cj[0][k + 1] = t4.y; cj[0][k + 2] = t4.z; cj[0][k + 3] = t4.w;
+          }
+        } else {
 #pragma unroll
-          for (int u = 0; u < JU; ++u) cj[u][k] = v[u];
+          for (int k = 0; k < NC; ++k) {
+            T v[JU];
+            ColVec<T, JU>::load(&tile[buf][k][jj], v);
+#pragma unroll
+            for (int u = 0; u < JU; ++u) cj[u][k] = v[u];
+          }
         }
         if constexpr (!PACKED) {
 #pragma unroll
@@ -585,7 +610,10 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       if constexpr (!BULK) {
         if (more) {
 #pragma unroll
-          for (int k = 0; k < NC; ++k) tile[buf ^ 1][k][tid] = stage[k];
+          for (int k = 0; k < NC; ++k) {
+            if constexpr (AOS) tile[buf ^ 1][tid][k] = stage[k];
+            else tile[buf ^ 1][k][tid] = stage[k];
+          }
         }
       }
       __syncthreads();

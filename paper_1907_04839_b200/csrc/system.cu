@@ -49,6 +49,8 @@ KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
     case 3: return make_choice<float, 3, kFwd, 2, 1, 7, true, 4>("fwd_f32x2_r2_j1_b7_u4");
     case 4: return LMS_PICK2(3, kFwd, 4, 2, 4, "fwd_f32x2_r4_j2");
     case 5: return make_choice<float, 3, kFwd, 2, 4, 7, true, 1, true>("fwd_f32x2_r2_j4_b7_tma");
+    case 8: return LMS_PICK2(3, kFwd, 4, 4, 4, "fwd_f32x2_r4_j4_b4");
+    case 9: return LMS_PICK2(3, kFwd, 4, 4, 3, "fwd_f32x2_r4_j4_b3");
     default: return LMS_PICK2(3, kFwd, 2, 4, 7, "fwd_f32x2_r2_j4_b7");
   }
 }
@@ -61,6 +63,11 @@ KernelChoice<float> pick_kernel<float, 3, kAdj>(int v)
     case 3: return make_choice<float, 3, kAdj, 2, 1, 4, true, 2>("adj_f32x2_r2_j1_b4_u2");
     case 4: return LMS_PICK2(3, kAdj, 4, 1, 3, "adj_f32x2_r4_j1");
     case 5: return make_choice<float, 3, kAdj, 2, 2, 5, true, 2, true>("adj_f32x2_r2_j2_b5_u2_tma");
+    case 6: return make_choice<float, 3, kAdj, 2, 1, 5, true, 4, false, true>("adj_f32x2_r2_aos_b5_u4");
+    case 7: return make_choice<float, 3, kAdj, 2, 1, 6, true, 4, false, true>("adj_f32x2_r2_aos_b6_u4");
+    case 8: return make_choice<float, 3, kAdj, 4, 1, 4, true, 2, false, true>("adj_f32x2_r4_aos_b4_u2");
+    case 9: return make_choice<float, 3, kAdj, 4, 1, 3, true, 4, false, true>("adj_f32x2_r4_aos_b3_u4");
+    case 10: return make_choice<float, 3, kAdj, 2, 1, 6, true, 8, false, true>("adj_f32x2_r2_aos_b6_u8");
     default: return make_choice<float, 3, kAdj, 2, 2, 5, true, 2>("adj_f32x2_r2_j2_b5_u2");
   }
 }
@@ -139,6 +146,7 @@ System<T, D>::System(const lms_config& c, int batch_count)
   LMS_CUDA(cudaGetDeviceProperties(&prop, c.device));
   if (prop.major != 10) throw StatusError{LMS_ERR_CUDA, "device is not sm_100 (B200); no fallback path exists"};
   num_sms_ = prop.multiProcessorCount;
+  if (const char* e = std::getenv("LMS_PDL")) pdl_ = std::atoi(e) != 0;
   LMS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   LMS_CUDA(cudaEventCreate(&ev_begin_));
   LMS_CUDA(cudaEventCreate(&ev_end_));
@@ -332,8 +340,22 @@ void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchP
   a.max_seg = plan.max_seg;
   a.partials = partials_;
   a.counters = counters_;
-  k.fn<<<plan.grid, kThreads, 0, stream_>>>(a);
-  LMS_CUDA(cudaGetLastError());
+  if (pdl_) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(plan.grid);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = stream_;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    LMS_CUDA(cudaLaunchKernelEx(&lc, k.fn, a));
+  } else {
+    k.fn<<<plan.grid, kThreads, 0, stream_>>>(a);
+    LMS_CUDA(cudaGetLastError());
+  }
   ++last_eval_launches;
 }
 

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -92,6 +93,9 @@ class SystemBase {
   virtual void final_q_batch(double* out) = 0;
   virtual cudaStream_t stream_handle() const = 0;
   int batch = 1;
+  // scratch owned by the device-resident L-BFGS driver (device_lbfgs.cu), kept across lms_register_device calls:
+  // cudaMalloc / cudaFree cost milliseconds (and synchronise the device) next to an 8 ms evaluation
+  std::shared_ptr<void> lbfgs_workspace;
 
   lms_config cfg{};
   int last_diverged_step = -1;
@@ -116,11 +120,12 @@ struct KernelChoice {
   const char* name = "";
 };
 
-template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false>
+template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false,
+          bool AOS = false>
 KernelChoice<T> make_choice(const char* name)
 {
   KernelChoice<T> c;
-  c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK>;
+  c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS>;
   c.rows_per_thread = R;
   c.name = name;
   return c;
@@ -195,6 +200,10 @@ class System final : public SystemBase {
 
   cudaStream_t stream_ = nullptr;
   int num_sms_ = 0;
+  // programmatic dependent launch between the pair kernels: opt-in (LMS_PDL=1).  Measured on B200 inside the
+  // evaluation graph: no gain at N >= 10 000 (8.088 vs 8.085 ms) and a loss at N = 2000..5000 (0.28 vs 0.25 ms),
+  // where the early-scheduled CTAs of the next step compete with the running one.
+  bool pdl_ = false;
   long long stride_ = 0;
   long long bs_traj_ = 0;   // elements between consecutive problems' trajectories
   long long bs_state_ = 0;  // ... between their (alpha,beta) states
