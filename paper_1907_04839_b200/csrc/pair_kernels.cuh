@@ -73,7 +73,7 @@ struct PairArgs {
   int* counters;
   int max_seg;
   // constants, rounded on the host exactly as the reference rounds them (shooting.hpp:63-68,114-115,
-  // 196,293): kexp = k_scale * log2(e) for float (ex2.approx), k_scale * log2(e) * 16 for double (Math<double>).
+  // 196,293): kexp = k_scale * log2(e) for float (ex2.approx), k_scale * log2(e) * 2^kExpBits for double (Math<double>).
   T kexp;
   T inv_sig2;
   T dt;
@@ -107,39 +107,76 @@ struct Math<float> {
   static __device__ __forceinline__ bool finite(float a) { return isfinite(a); }
 };
 
-// 2^(j/16), j = 0..15, correctly rounded (generated with 60-digit decimal arithmetic).
-__device__ __constant__ double kExp2Table[16] = {
-    0x1.0000000000000p+0, 0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0, 0x1.2387a6e756238p+0,
-    0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0, 0x1.4bfdad5362a27p+0, 0x1.5ab07dd485429p+0,
-    0x1.6a09e667f3bcdp+0, 0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0, 0x1.9c49182a3f090p+0,
-    0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0, 0x1.ea4afa2a490dap+0};
+// fp64 exp: table of 2^(j/2^B) and a near-minimax polynomial for 2^(g/2^B) on g in [-1/2, 1/2] (mpmath chebyfit,
+// 50 digits, coefficients rounded to double; constant term exactly 1 so that K(r = 0) = 1).  LMS_EXP_BITS selects
+//   4: 16 entries (128 B: every bank once, conflict-free for any index pattern), degree 6, |rel err| < 7.9e-18
+//   5: 32 entries, degree 5, < 1.5e-16        6: 64 entries, degree 4, < 2.5e-15
+// A larger table trades DP-pipe work (one DFMA per step) for shared-memory bank conflicts on the table load.
+// Measured on B200 (N = 20 000, T = 10 gradient; scripts/gpu_exp_ab.sh): 22.33 / 21.90 / 21.64 ms for B = 4 / 5 / 6
+// (degree 7 with 16 entries, the first version: 22.85 ms).  Default 5: the last setting below half an ulp.
+#ifndef LMS_EXP_BITS
+#define LMS_EXP_BITS 5
+#endif
+constexpr int kExpBits = LMS_EXP_BITS;
+constexpr int kExpEntries = 1 << kExpBits;
+// 2^(j/64), j = 0..63, correctly rounded; the smaller tables take every 2nd / 4th entry.
+__device__ __constant__ double kExp2Table64[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
 
 template <>
 struct Math<double> {
-  // exp(r2 * k_scale) for r2 * k_scale <= 0, branch-free.  kexp = k_scale * log2(e) * 16 (host, one
-  // rounding), s = r2 * kexp; 2^(s/16) = 2^n * 2^(j/16) * 2^(g/16) with 16 n + j = rint(s), g = s - rint(s)
-  // in [-1/2, 1/2]: a 16-entry shared-memory table (16 x 8 B spans the 32 banks exactly once: conflict-free
-  // for any index pattern) and a degree-7 polynomial (truncation 1.2e-18).  13 DP-pipe operations against
-  // the 18 of CUDA's exp(), and no slow path: with landmarks many sigma apart most pairs underflow, which
-  // is exactly where the library routine branches.  Results below the normal range flush to zero.
+  // exp(r2 * k_scale) for r2 * k_scale <= 0, branch-free.  kexp = k_scale * log2(e) * 2^B (host, one rounding),
+  // s = r2 * kexp; 2^(s/2^B) = 2^n * 2^(j/2^B) * 2^(g/2^B) with 2^B n + j = rint(s), g = s - rint(s) in
+  // [-1/2, 1/2].  With B = 5: 11 DP-pipe operations against the 18 of CUDA's exp(), and no slow path: with
+  // landmarks many sigma apart most pairs underflow, which is exactly where the library routine branches.
+  // Results below the normal range flush to zero.
   static __device__ __forceinline__ double kernel(double r2, double kexp, const double* __restrict__ tbl)
   {
     double s = r2 * kexp;
-    s = s < -17280.0 ? -17280.0 : s;  // 2^-1080; a NaN argument falls through and propagates
+    constexpr double floor_s = -1080.0 * kExpEntries;  // 2^-1080; a NaN argument falls through and propagates
+    s = s < floor_s ? floor_s : s;
     const double magic = 6755399441055744.0;  // 1.5 * 2^52: the low word of (s + magic) is rint(s)
     const double km = __dadd_rn(s, magic);
     const int ki = __double2loint(km);
     const double g = s - __dadd_rn(km, -magic);
-    double p = 0x1.ffcbfc588b0c7p-45;          // (ln2/16)^k / k!, k = 7 .. 1
-    p = fma(p, g, 0x1.430912f86c787p-37);
-    p = fma(p, g, 0x1.5d87fe78a6731p-30);
-    p = fma(p, g, 0x1.3b2ab6fba4e77p-23);
-    p = fma(p, g, 0x1.c6b08d704a0c0p-17);
-    p = fma(p, g, 0x1.ebfbdff82c58fp-11);
-    p = fma(p, g, 0x1.62e42fefa39efp-5);
+    double p;
+    if constexpr (kExpBits == 4) {
+      p = 0x1.430a49610efc6p-37;
+      p = fma(p, g, 0x1.5d89be4c12513p-30);
+      p = fma(p, g, 0x1.3b2ab6fb09b31p-23);
+      p = fma(p, g, 0x1.c6b08d6e8a384p-17);
+      p = fma(p, g, 0x1.ebfbdff82c594p-11);
+      p = fma(p, g, 0x1.62e42fefa39fdp-5);
+    } else if constexpr (kExpBits == 5) {
+      p = 0x1.5d885e6ef14a6p-35;
+      p = fma(p, g, 0x1.3b2b301f1eb9cp-27);
+      p = fma(p, g, 0x1.c6b08d70380ddp-20);
+      p = fma(p, g, 0x1.ebfbdff7feebap-13);
+      p = fma(p, g, 0x1.62e42fefa39efp-6);
+    } else {
+      p = 0x1.3b2ad0385b409p-31;
+      p = fma(p, g, 0x1.c6b0c40d8c4e9p-23);
+      p = fma(p, g, 0x1.ebfbdff82ac52p-15);
+      p = fma(p, g, 0x1.62e42fefa0352p-7);
+    }
     p = fma(p, g, 1.0);
-    const double r = tbl[ki & 15] * p;
-    const int n = ki >> 4;
+    const double r = tbl[ki & (kExpEntries - 1)] * p;
+    const int n = ki >> kExpBits;
     const double scaled = __hiloint2double(__double2hiint(r) + n * 1048576, __double2loint(r));
     return n < -1021 ? 0.0 : scaled;
   }
@@ -425,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 
   __shared__ __align__(16) T tile[2][AOS ? kTileJ : NC][AOS ? NC : kTileJ];
   __shared__ double red_scratch[kThreads];
-  __shared__ double exp_tbl[16];  // fp64 only: 2^(j/16) for Math<double>::kernel
+  __shared__ double exp_tbl[kExpEntries];  // fp64 only: 2^(j/2^B) for Math<double>::kernel
   __shared__ int s_last;
   __shared__ __align__(8) unsigned long long tile_bar[2];  // BULK only: one mbarrier per tile buffer
   // Programmatic dependent launch: the next launch of the evaluation may start scheduling its CTAs as soon as
@@ -443,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     __syncthreads();
   }
   if constexpr (sizeof(T) == 8) {
-    if (threadIdx.x < 16) exp_tbl[threadIdx.x] = kExp2Table[threadIdx.x];
+    if (threadIdx.x < kExpEntries) exp_tbl[threadIdx.x] = kExp2Table64[threadIdx.x * (64 / kExpEntries)];
     __syncthreads();
   }
 

@@ -157,7 +157,7 @@ System<T, D>::System(const lms_config& c, int batch_count)
   if constexpr (sizeof(T) == 4)
     kexp_ = (T)((double)k_scale * 1.4426950408889634074);  // ex2.approx: exp(x) = 2^(x log2 e)
   else
-    kexp_ = (T)((long double)k_scale * 23.08312065422341418507L);  // log2(e) * 16, see Math<double>::kernel
+    kexp_ = (T)((long double)k_scale * 1.44269504088896340735992468100189214L * (long double)kExpEntries);  // Math<double>::kernel
 
   k_fwd_ = pick_kernel<T, D, kFwd>(c.variant);
   k_adj_ = pick_kernel<T, D, kAdj>(c.variant);
