@@ -265,11 +265,25 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   int per_sm = 0;
   LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kThreads, 0));
   per_sm = std::max(per_sm, 1);
+  static const int cap_per_sm = [] {
+    const char* e = std::getenv("LMS_CTAS_PER_SM");  // experiment knob: cap on resident CTAs per SM
+    return e ? std::max(std::atoi(e), 1) : 1 << 20;
+  }();
+  per_sm = std::min(per_sm, cap_per_sm);
   const long long full = (long long)num_sms_ * per_sm;
   // Never more CTAs than staged tiles: a CTA sweeps at least one full tile's worth of columns.  (Measured:
   // going finer -- 32 columns per CTA -- makes N = 1000..2000 slower, 0.30 -> 0.43 ms and 0.35 -> 0.88 ms per
   // gradient: the partial-slot write / fence / counter / re-read chain costs more than the extra parallelism.)
-  p.grid = (int)std::min<long long>(full, std::max<long long>(cells / kUnitsPerTile, 1));
+  static const int min_units = [] {
+    const char* e = std::getenv("LMS_MIN_UNITS");  // experiment knob: work units (8 columns) a CTA sweeps at least
+    return e ? std::max(std::atoi(e), 1) : kUnitsPerTile;
+  }();
+  p.grid = (int)std::min<long long>(full, std::max<long long>(cells / min_units, 1));
+  // The last CTA of a row tile adds that tile's grid / n_row_tiles partial segments one after the other (an L2
+  // round trip per few segments).  Measured on B200 (N = 5000: 0.795 -> 0.727 ms, N = 7000: 1.240 -> 1.213 ms per
+  // gradient): beyond ~20 segments the serial chain costs more than the occupancy it buys, down to 2 CTAs per SM
+  // (N = 20 000 runs only 3.5 % slower at 3 CTAs per SM than at 7).
+  p.grid = (int)std::min<long long>(p.grid, std::max<long long>(2LL * num_sms_, 20LL * p.n_row_tiles));
   // mid-size problems: a whole number of CTAs per SM, so no SM carries one CTA more than its neighbours
   if (p.grid < full && p.grid > num_sms_) p.grid -= p.grid % num_sms_;
   // partial slots are indexed (row tile, segment): a row tile is shared by at most max_seg CTAs, since every
