@@ -1,6 +1,18 @@
 """Error taxonomy of the reference (errors.hpp:10-77), raised from C-ABI status codes."""
 
 
+class IoError(RuntimeError):
+    """File/stream level failure: missing file, unwritable destination (errors.hpp:10-13)."""
+
+
+class ParseError(RuntimeError):
+    """Malformed input data; carries a 1-based line number when known (errors.hpp:16-28)."""
+
+    def __init__(self, msg, line=0):
+        super().__init__(f"{msg} at line {line}" if line else msg)
+        self.line = line
+
+
 class ShapeError(RuntimeError):
     """Mismatched landmark counts/dimensions (errors.hpp:31-34)."""
 
