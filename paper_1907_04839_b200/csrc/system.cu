@@ -278,14 +278,22 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
     const char* e = std::getenv("LMS_MIN_UNITS");  // experiment knob: work units (8 columns) a CTA sweeps at least
     return e ? std::max(std::atoi(e), 1) : kUnitsPerTile;
   }();
-  p.grid = (int)std::min<long long>(full, std::max<long long>(cells / min_units, 1));
+  // ... except when even that leaves half the SMs idle: then half tiles (N = 1000: 0.231 -> 0.194 ms per gradient,
+  // N = 1500: 0.241 -> 0.221 ms; from N = 2000 on whole tiles are faster again, 0.248 vs 0.304 ms).
+  const long long tiles = cells / kUnitsPerTile;
+  const int units = (min_units == kUnitsPerTile && 2 * tiles <= num_sms_) ? kUnitsPerTile / 2 : min_units;
+  p.grid = (int)std::min<long long>(full, std::max<long long>(cells / units, 1));
   // The last CTA of a row tile adds that tile's grid / n_row_tiles partial segments one after the other (an L2
   // round trip per few segments).  Measured on B200 (N = 5000: 0.795 -> 0.727 ms, N = 7000: 1.240 -> 1.213 ms per
   // gradient): beyond ~20 segments the serial chain costs more than the occupancy it buys, down to 2 CTAs per SM
   // (N = 20 000 runs only 3.5 % slower at 3 CTAs per SM than at 7).
   p.grid = (int)std::min<long long>(p.grid, std::max<long long>(2LL * num_sms_, 20LL * p.n_row_tiles));
   // mid-size problems: a whole number of CTAs per SM, so no SM carries one CTA more than its neighbours
-  if (p.grid < full && p.grid > num_sms_) p.grid -= p.grid % num_sms_;
+  static const int round_from = [] {
+    const char* e = std::getenv("LMS_ROUND_FROM");  // experiment knob: round only grids of at least this many CTAs per SM
+    return e ? std::max(std::atoi(e), 1) : 1;
+  }();
+  if (p.grid < full && p.grid > (long long)round_from * num_sms_) p.grid -= p.grid % num_sms_;
   // partial slots are indexed (row tile, segment): a row tile is shared by at most max_seg CTAs, since every
   // CTA owns at least floor(cells / grid) consecutive units
   const long long per_cta_min = std::max<long long>(cells / p.grid, 1);
