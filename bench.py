@@ -30,6 +30,9 @@ if ROOT not in sys.path:
 SIGMA, LAMBDA = 1.5, 5e5  # shooting.hpp:26-28
 FWD_SLOTS, ADJ_SLOTS = 18, 43  # FP32 lane-instructions per pair, SURVEY.md §8d (fp64: 35 / 60)
 FWD_SLOTS_F64, ADJ_SLOTS_F64 = 35, 60
+# CPU arm: the reference's compute_gradient on a sample of the workload at the same landmark density; N = 6000 is
+# (2T+2) * 3.6e7 pair evaluations = about 1 s per gradient on 16 host threads, 15-20 core-seconds of CPU work
+CPU_SAMPLE_N = 6000
 
 
 def parse_args():
@@ -174,16 +177,20 @@ def reference_arm(args):
     if rank != 0:
         return
     T = args.timesteps or 10
-    n_sample = args.n or 3000
+    n = 20000 if args.gpus == 1 else 200000  # the workload our own arm measures at this --gpus
+    n_sample = args.n or CPU_SAMPLE_N
     res = cpu_reference_run(n_sample, T, args.precision, max(args.steps, 1), max(args.warmup, 0))
     line = {
         "impl": "reference", "metric": "pair_kernel_evals_per_sec_per_gradient", "value": res["value"],
         "unit": "pair-evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": res["sec_per_gradient"] * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-        "config": {"workload": f"single registration, reference CPU compute_gradient, N={n_sample}, T={T} "
-                               f"(bounded sample of the N=20000 workload)", "n": n_sample, "timesteps": T,
-                   "sigma": SIGMA, "lambda": LAMBDA},
+        # our arm's workload; every step times the reference on a bounded sample of it (same generator, same
+        # landmark density, same T, sigma, lambda), throughput counted in the same unit
+        "config": {"workload": f"single registration N={n}, T={T}, one fwd+bwd gradient per step", "n": n,
+                   "timesteps": T, "sigma": SIGMA, "lambda": LAMBDA, "units_per_step": "2*T*N^2",
+                   "template": "Fibonacci sphere, radius 20*sqrt(N/1847) mm (constant landmark density)",
+                   "sample": res["sample"], "n_sample": n_sample},
         "cpu_baseline": {"value": res["value"], "unit": "pair-evals/s", "cores": res["cores"], "kind": res["kind"],
                          "sample": res["sample"]},
         "e2e": {"value": res["value"], "unit": "pair-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -397,7 +404,7 @@ def b200_arm(args):
                                         "ms_per_iteration": (lbd_ms - dev_ms / K) / max(regd.iterations, 1),
                                         "ms_total": lbd_ms, "final_loss": regd.final_loss}
         try:
-            cpu = cpu_reference_run(3000, T, prec, 1, 1)
+            cpu = cpu_reference_run(CPU_SAMPLE_N, T, prec, 1, 1)
             line["cpu_baseline"] = {"value": cpu["value"], "unit": "pair-evals/s", "cores": cpu["cores"],
                                     "kind": cpu["kind"], "sample": cpu["sample"]}
         except Exception as e:  # the oracle is test infrastructure; its absence must not hide the GPU number

@@ -25,8 +25,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// segments of partial sums whose loads are in flight together in the last CTA's combine loop
+#ifndef LMS_COMBINE_UNROLL
+#define LMS_COMBINE_UNROLL 4
+#endif
+
 namespace lms {
 
+constexpr int kCombineUnroll = LMS_COMBINE_UNROLL;
 constexpr int kThreads = 128;  // threads per CTA
 constexpr int kTileJ = 128;    // columns staged per shared-memory tile
 constexpr int kUnitJ = 8;      // stream-K work unit: kUnitJ columns of one row tile
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
           for (int k = 0; k < NA; ++k) acc[r][k] = T(0);
         // ascending segment order = ascending columns; loads of several segments are in flight together
         const T* seg0 = a.partials + rt_local * a.max_seg * (long long)(NA * BM);
-#pragma unroll 4
+#pragma unroll kCombineUnroll
         for (int ord = 0; ord < nseg; ++ord) {
           const T* theirs = seg0 + (long long)ord * (NA * BM);
 #pragma unroll
