@@ -46,6 +46,8 @@ def parse_args():
     ap.add_argument("--timesteps", type=int, default=0)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--mode", default="rows", choices=["rows", "replicas"])
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="rows mode: per-step NCCL all-gather, or peer stores from the kernel epilogues + stream flags")
     ap.add_argument("--batch", type=int, default=0, help="population mode: B registrations of --n landmarks per GPU")
     ap.add_argument("--no-extras", action="store_true", help="skip fp64, L-BFGS and cpu_baseline legs")
     ap.add_argument("--lbfgs-iters", type=int, default=30)
@@ -237,7 +239,11 @@ def b200_arm(args):
     x0 = np.ascontiguousarray(((target - q0) / T).ravel())
 
     system = HamiltonianSystem(SIGMA, n, 3, prec, device=local_rank, max_timesteps=T, variant=args.variant)
-    if rows_mode:
+    if rows_mode and args.exchange == "p2p":
+        blobs = [None] * world
+        dist.all_gather_object(blobs, system.p2p_export(rank, world))
+        system.p2p_connect(blobs)
+    elif rows_mode:
         uid = [comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         system.comm_init(uid[0], rank, world)
@@ -301,8 +307,9 @@ def b200_arm(args):
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True,
         "scaling": "strong" if rows_mode else "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
         "config": {
-            "workload": (f"single registration N={n}, T={T}, row-partitioned over {world} GPUs, per-step NCCL "
-                         f"all-gather" if rows_mode else
+            "workload": (f"single registration N={n}, T={T}, row-partitioned over {world} GPUs, per-step "
+                         + ("NCCL all-gather" if args.exchange == "nccl" else "peer-push exchange (P2P stores + flags)")
+                         if rows_mode else
                          f"single registration N={n}, T={T}, one fwd+bwd gradient per step"
                          + (f", {world} independent replicas" if distributed else "")),
             "n": n, "timesteps": T, "sigma": SIGMA, "lambda": LAMBDA, "units_per_step": "2*T*N^2",

@@ -226,6 +226,18 @@ int lms_local_group_create(int world, lms_local_group** out);
 void lms_local_group_destroy(lms_local_group* group);
 int lms_system_join_local_group(lms_system* sys, lms_local_group* group, int rank);
 
+/* Peer-push transport for the same row partition: instead of an all-gather after every time step, the kernels'
+ * epilogues store each updated row straight into every peer's memory (NVLink peer stores between GPUs; CUDA IPC
+ * mappings between processes) while the rest of the step is still being computed, and only a 4-byte arrival flag
+ * per peer is exchanged in stream order (cuStreamWriteValue32 / cuStreamWaitValue32).  Up to 8 ranks.
+ *   1. every rank:  lms_p2p_export(sys, rank, world, blob)      -- lays the handle out for `world` ranks
+ *   2. the application all-gathers the `world` blobs (rank-major, LMS_P2P_BLOB_BYTES each)
+ *   3. every rank:  lms_p2p_connect(sys, blobs)                 -- then lms_bind_registration / lms_objective_eval
+ * Ranks may be processes (one per GPU, or several on one GPU) or handles of one process. */
+#define LMS_P2P_BLOB_BYTES 128
+int lms_p2p_export(lms_system* sys, int rank, int world, unsigned char blob[LMS_P2P_BLOB_BYTES]);
+int lms_p2p_connect(lms_system* sys, const unsigned char* blobs);
+
 /* ---- synthetic inputs (synth.hpp:15-43, rng.hpp) ---- */
 
 /* Rng(seed).normal() / uniform() streams (rng.hpp:19-41; std::mt19937_64). */

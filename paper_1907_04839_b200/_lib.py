@@ -103,6 +103,8 @@ SIGNATURES = {
     "lms_local_group_create": ([c_int, POINTER(c_void_p)], c_int),
     "lms_local_group_destroy": ([c_void_p], None),
     "lms_system_join_local_group": ([c_void_p, c_void_p, c_int], c_int),
+    "lms_p2p_export": ([c_void_p, c_int, c_int, POINTER(c_ubyte)], c_int),
+    "lms_p2p_connect": ([c_void_p, POINTER(c_ubyte)], c_int),
     "lms_rng_normals": ([c_uint64, c_size_t, _dp], None),
     "lms_rng_uniforms": ([c_uint64, c_size_t, _dp], None),
     "lms_synth_sphere": ([c_size_t, c_double, _dp], None),

@@ -309,6 +309,18 @@ int lms_system_comm_init(lms_system* sys, const unsigned char id[128], int rank,
   return guarded(sys, [&](lms::SystemBase* s) { s->comm_init(id, rank, world); });
 }
 
+int lms_p2p_export(lms_system* sys, int rank, int world, unsigned char blob[LMS_P2P_BLOB_BYTES])
+{
+  if (!blob) return LMS_ERR_INVALID;
+  return guarded(sys, [&](lms::SystemBase* s) { s->p2p_export(rank, world, blob); });
+}
+
+int lms_p2p_connect(lms_system* sys, const unsigned char* blobs)
+{
+  if (!blobs) return LMS_ERR_INVALID;
+  return guarded(sys, [&](lms::SystemBase* s) { s->p2p_connect(blobs); });
+}
+
 // ---- register_impl core (registration.cpp:43-93) over the bound objective and lms_minimize ----
 static double bound_objective(void* user, const double* x, double* grad, size_t)
 {

@@ -37,6 +37,7 @@ constexpr int kThreads = 128;  // threads per CTA
 constexpr int kTileJ = 128;    // columns staged per shared-memory tile
 constexpr int kUnitJ = 8;      // stream-K work unit: kUnitJ columns of one row tile
 constexpr int kUnitsPerTile = kTileJ / kUnitJ;
+constexpr int kMaxPeers = 7;   // row partition: up to 8 GPUs of one NVSwitch domain
 
 enum Mode : int { kFwd = 0, kAdj = 1, kVel = 2 };
 
@@ -92,7 +93,21 @@ struct PairArgs {
   int tiles_per_problem;
   const int* batch_ids;
   long long bs_j, bs_adj, bs_out, bs_seed, bs_vec, bs_grad, bs_part, bs_div;
+  // Row partition with the peer-push exchange (system.cu, p2p_*): every store of the Euler epilogues (new state,
+  // adjoint seed, gradient, scalar partials) also goes to the same offset of each peer's exchange arena -- over
+  // NVLink when the peer is another GPU -- so the updated slice travels while the other row tiles are still
+  // being computed and no gather kernel follows.  n_peers == 0: single GPU, or the NCCL / loopback transports.
+  int n_peers;
+  long long peer_delta[kMaxPeers];  // byte distance from this rank's arena to each peer's mapping of its arena
 };
+
+// One value to the local buffer and to the same place in every peer's arena.
+template <typename T, typename V>
+__device__ __forceinline__ void put_all(const PairArgs<T>& a, V* p, V v)
+{
+  *p = v;
+  for (int k = 0; k < a.n_peers; ++k) *reinterpret_cast<V*>(reinterpret_cast<char*>(p) + a.peer_delta[k]) = v;
+}
 
 // ---------------------------------------------------------------------------------------------
 // scalar math per working precision
@@ -766,8 +781,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
                 qn[k] = Math<T>::add_rn(ri[r][k], Math<T>::mul_rn(a.dt, hp[k]));
                 const T pn = Math<T>::add_rn(ri[r][D + k], -Math<T>::mul_rn(a.dt, hq[k]));
                 ok = ok && Math<T>::finite(qn[k]) && Math<T>::finite(pn);
-                out_b[(long long)k * a.ostride + row] = qn[k];
-                out_b[(long long)(D + k) * a.ostride + row] = pn;
+                put_all(a, &out_b[(long long)k * a.ostride + row], qn[k]);
+                put_all(a, &out_b[(long long)(D + k) * a.ostride + row], pn);
               }
               if (!ok) atomicMin(diverged_b, ((unsigned long long)(unsigned)a.step << 32) | 0xffffffffull);
               if (a.epi & kEpiFirstStep) {
@@ -784,8 +799,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
                   const double df = (double)qn[k] - (double)tg;  // shooting.hpp:324-325
                   msum += df * df;
                   // alpha_T = 2*lambda*(q(1) - target), beta_T = 0   (shooting.hpp:290-296)
-                  adj_seed_b[(long long)k * a.ostride + row] = Math<T>::mul_rn(a.two_lambda, qn[k] - tg);
-                  adj_seed_b[(long long)(D + k) * a.ostride + row] = T(0);
+                  put_all(a, &adj_seed_b[(long long)k * a.ostride + row], Math<T>::mul_rn(a.two_lambda, qn[k] - tg));
+                  put_all(a, &adj_seed_b[(long long)(D + k) * a.ostride + row], T(0));
                 }
               }
             } else {
@@ -807,11 +822,11 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
                 // alpha += dt*d_alpha ; beta += dt*d_beta   (shooting.hpp:302-306)
                 const T an = Math<T>::add_rn(ri[r][2 * D + k], Math<T>::mul_rn(a.dt, da));
                 const T bn = Math<T>::add_rn(ri[r][3 * D + k], Math<T>::mul_rn(a.dt, dbeta));
-                out_b[(long long)k * a.ostride + row] = an;
-                out_b[(long long)(D + k) * a.ostride + row] = bn;
+                put_all(a, &out_b[(long long)k * a.ostride + row], an);
+                put_all(a, &out_b[(long long)(D + k) * a.ostride + row], bn);
                 if (a.epi & kEpiGradOut)  // grad = beta_0 + hp(q0,p0)   (shooting.hpp:311-313)
-                  grad_out_b[row * D + k] =
-                      (double)Math<T>::add_rn(bn, hp0_b[(long long)k * a.ostride + row]);
+                  put_all(a, &grad_out_b[row * D + k],
+                          (double)Math<T>::add_rn(bn, hp0_b[(long long)k * a.ostride + row]));
               } else {
                 out_b[(long long)k * a.ostride + row] = da;
                 out_b[(long long)(D + k) * a.ostride + row] = dbeta;
@@ -824,11 +839,11 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         // block-uniform flags: every thread takes the same branch around the barriers in block_sum
         if (a.epi & kEpiFirstStep) {
           const double h = block_sum(hsum, red_scratch);
-          if (tid == 0) h_part_b[(long long)rt * R] = h;  // indexed in 128-row units
+          if (tid == 0) put_all(a, &h_part_b[(long long)rt * R], h);  // indexed in 128-row units
         }
         if (a.epi & kEpiLastStep) {
           const double m = block_sum(msum, red_scratch);
-          if (tid == 0) mm_part_b[(long long)rt * R] = m;
+          if (tid == 0) put_all(a, &mm_part_b[(long long)rt * R], m);
         }
       }
     }

@@ -1,6 +1,9 @@
 // System<T,D>: implementation.  See system.cuh.
 #include "system.cuh"
 
+#include <unistd.h>
+
+#include <cstdint>
 #include <cstdlib>
 
 namespace lms {
@@ -171,9 +174,6 @@ System<T, D>::System(const lms_config& c, int batch_count)
   bs_traj_ = (long long)(max_t_ + 1) * kState * stride_;
   bs_state_ = (long long)kState * stride_;
   bs_vec_ = (long long)D * stride_;
-  traj_ = dev_alloc_zero<T>(B * (size_t)bs_traj_);
-  adj_[0] = dev_alloc_zero<T>(B * kState * plane);
-  adj_[1] = dev_alloc_zero<T>(B * kState * plane);
   hp0_ = dev_alloc_zero<T>(B * D * plane);
   target_ = dev_alloc_zero<T>(B * D * plane);
   q0_ = dev_alloc_zero<T>(B * D * plane);
@@ -184,12 +184,34 @@ System<T, D>::System(const lms_config& c, int batch_count)
   io_cap_ = (size_t)N * D * B;
   d_io_ = dev_alloc_zero<double>(4 * io_cap_);
   d_x_ = dev_alloc_zero<double>(std::max((size_t)stride_ * D, B * (size_t)N * D));
-  d_grad_ = dev_alloc_zero<double>(std::max((size_t)stride_ * D, B * (size_t)N * D));
   d_ids_ = dev_alloc_zero<int>(B);
   LMS_CUDA(cudaMallocHost(&h_scalars_, 4 * B * sizeof(double)));
   part_tiles_ = (int)(stride_ / kThreads);
-  h_part_ = dev_alloc_zero<double>(B * part_tiles_);
-  mm_part_ = dev_alloc_zero<double>(B * part_tiles_);
+  alloc_exchange_arena();
+}
+
+// traj_, adj_[0..1], d_grad_, h_part_, mm_part_ and the exchange flags in one allocation (see p2p_export).
+template <typename T, int D>
+void System<T, D>::alloc_exchange_arena()
+{
+  const size_t B = (size_t)batch;
+  const size_t plane = (size_t)stride_;
+  auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t b_traj = up(B * (size_t)bs_traj_ * sizeof(T));
+  const size_t b_adj = up(B * kState * plane * sizeof(T));
+  const size_t b_grad = up(std::max(plane * D, B * (size_t)cfg.n * D) * sizeof(double));
+  const size_t b_part = up(B * (size_t)part_tiles_ * sizeof(double));
+  const size_t b_flags = 256;
+  arena_bytes_ = b_traj + 2 * b_adj + b_grad + 2 * b_part + b_flags;
+  arena_ = dev_alloc_zero<char>(arena_bytes_);
+  char* p = arena_;
+  traj_ = reinterpret_cast<T*>(p);            p += b_traj;
+  adj_[0] = reinterpret_cast<T*>(p);          p += b_adj;
+  adj_[1] = reinterpret_cast<T*>(p);          p += b_adj;
+  d_grad_ = reinterpret_cast<double*>(p);     p += b_grad;
+  h_part_ = reinterpret_cast<double*>(p);     p += b_part;
+  mm_part_ = reinterpret_cast<double*>(p);    p += b_part;
+  p2p_flags_ = reinterpret_cast<unsigned*>(p);
 }
 
 template <typename T, int D>
@@ -199,9 +221,8 @@ System<T, D>::~System()
   if (stream_) cudaStreamSynchronize(stream_);
   destroy_graph();
   if (comm_ && nccl_api().ok) nccl_api().CommDestroy(comm_);
-  dev_free(traj_);
-  dev_free(adj_[0]);
-  dev_free(adj_[1]);
+  p2p_disconnect();
+  dev_free(arena_);
   dev_free(hp0_);
   dev_free(target_);
   dev_free(q0_);
@@ -211,12 +232,9 @@ System<T, D>::~System()
   dev_free(points_[1]);
   dev_free(partials_);
   dev_free(counters_);
-  dev_free(h_part_);
-  dev_free(mm_part_);
   dev_free(d_scalars_);
   dev_free(d_io_);
   dev_free(d_x_);
-  dev_free(d_grad_);
   dev_free(d_ids_);
   if (h_scalars_) cudaFreeHost(h_scalars_);
   for (auto e : events_) cudaEventDestroy(e);
@@ -348,6 +366,7 @@ PairArgs<T> System<T, D>::base_args() const
   a.bs_grad = (long long)n() * D;
   a.bs_part = part_tiles_;
   a.bs_div = 4;
+  a.n_peers = 0;
   return a;
 }
 
@@ -355,6 +374,7 @@ template <typename T, int D>
 template <int MODE>
 void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchPlan& plan)
 {
+  p2p_dirty_ = true;  // a rank that owns no live rows launches nothing but still has to announce the step
   if (plan.grid <= 0) return;
   a.n_row_tiles = plan.n_row_tiles;
   a.tiles_per_problem = plan.tiles_per_problem;
@@ -663,6 +683,10 @@ void System<T, D>::enqueue_eval(bool timed, int count, const int* d_ids)
     ++last_eval_launches;
   }
   auto batch_strides = [&](PairArgs<T>& a, long long bs_out, long long bs_adj) {
+    if (p2p_active_) {
+      a.n_peers = n_peers_;
+      for (int k = 0; k < n_peers_; ++k) a.peer_delta[k] = peer_delta_[k];
+    }
     a.batch_ids = d_ids;
     a.bs_j = bs_traj_;
     a.bs_adj = bs_adj;
@@ -966,25 +990,20 @@ void System<T, D>::relayout_for_world(int world, int rank)
   if (new_stride != stride_) {
     stride_ = new_stride;
     const size_t plane = (size_t)stride_;
-    dev_free(traj_); dev_free(adj_[0]); dev_free(adj_[1]); dev_free(hp0_); dev_free(target_); dev_free(q0_);
-    dev_free(scratch_in_); dev_free(scratch_out_); dev_free(d_x_); dev_free(d_grad_); dev_free(h_part_);
-    dev_free(mm_part_);
+    p2p_disconnect();
+    dev_free(arena_); dev_free(hp0_); dev_free(target_); dev_free(q0_);
+    dev_free(scratch_in_); dev_free(scratch_out_); dev_free(d_x_);
     bs_traj_ = (long long)(max_t_ + 1) * kState * stride_;
     bs_state_ = (long long)kState * stride_;
     bs_vec_ = (long long)D * stride_;
-    traj_ = dev_alloc_zero<T>((size_t)(max_t_ + 1) * kState * plane);
-    adj_[0] = dev_alloc_zero<T>(kState * plane);
-    adj_[1] = dev_alloc_zero<T>(kState * plane);
     hp0_ = dev_alloc_zero<T>(D * plane);
     target_ = dev_alloc_zero<T>(D * plane);
     q0_ = dev_alloc_zero<T>(D * plane);
     scratch_in_ = dev_alloc_zero<T>(2 * kState * plane);
     scratch_out_ = dev_alloc_zero<T>(kState * plane);
     d_x_ = dev_alloc_zero<double>(plane * D);
-    d_grad_ = dev_alloc_zero<double>(plane * D);
     part_tiles_ = (int)(stride_ / kThreads);
-    h_part_ = dev_alloc_zero<double>(part_tiles_);
-    mm_part_ = dev_alloc_zero<double>(part_tiles_);
+    alloc_exchange_arena();
   }
   rank_ = rank;
   world_ = world;
@@ -1022,6 +1041,10 @@ void System<T, D>::join_local_group(LocalGroup* group, int rank)
 template <typename T, int D>
 void System<T, D>::gather_inplace(const std::vector<std::pair<char*, size_t>>& buffers)
 {
+  if (p2p_active_) {  // the epilogues already pushed every slice: only the arrival flags are exchanged
+    p2p_exchange();
+    return;
+  }
   if (local_ == nullptr) {
     const NcclApi& nc = nccl_api();
     bool ok = nc.GroupStart() == 0;
@@ -1075,6 +1098,145 @@ template <typename T, int D>
 void System<T, D>::all_gather_doubles(double* buf)
 {
   gather_inplace({{reinterpret_cast<char*>(buf), (size_t)(part_tiles_ / world_) * sizeof(double)}});
+}
+
+// ---- peer-push exchange ------------------------------------------------------------------------------------------
+// The third transport of the row partition (after NCCL and the in-process loopback).  Every rank maps every
+// peer's exchange arena -- cudaIpcOpenMemHandle across processes, the plain pointer inside one process (peer
+// access enabled when the devices differ) -- and the Euler epilogues of the pair kernels store each updated
+// row into all arenas (put_all, pair_kernels.cuh): the exchange of step t rides on the NVLink stores issued
+// while the remaining row tiles of step t are still being computed.  What is left of the all-gather is one
+// 4-byte flag per peer: after its launch a rank writes its epoch into every peer's flag slot in stream order
+// (cuStreamWriteValue32: fenced after the kernel's stores) and its stream waits until every peer's slot has
+// reached the epoch (cuStreamWaitValue32), so no SM ever spins.  Buffers cannot be overwritten early: a rank
+// only starts step s+1 after every peer has finished step s, and the two adjoint states / T+1 snapshots are
+// written in alternation.
+namespace {
+using StreamValueFn = int (*)(cudaStream_t, unsigned long long, unsigned, unsigned);
+struct StreamMemOps {
+  StreamValueFn write = nullptr, wait = nullptr;
+  bool ok = false;
+};
+const StreamMemOps& stream_mem_ops()
+{
+  static const StreamMemOps ops = [] {
+    StreamMemOps o;
+    void* w = nullptr;
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult rw, rq;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &rw) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &q, cudaEnableDefault, &rq) == cudaSuccess &&
+        rw == cudaDriverEntryPointSuccess && rq == cudaDriverEntryPointSuccess && w && q) {
+      o.write = reinterpret_cast<StreamValueFn>(w);
+      o.wait = reinterpret_cast<StreamValueFn>(q);
+      o.ok = true;
+    }
+    cudaGetLastError();
+    return o;
+  }();
+  return ops;
+}
+constexpr unsigned long long kBlobMagic = 0x4c4d53503250ull;  // "LMSP2P"
+}  // namespace
+
+template <typename T, int D>
+void System<T, D>::p2p_export(int rank, int world, unsigned char* blob)
+{
+  if (world < 1 || world > kMaxPeers + 1 || rank < 0 || rank >= world)
+    throw StatusError{LMS_ERR_INVALID, "bad rank/world (the peer-push exchange serves up to 8 ranks)"};
+  if (!stream_mem_ops().ok) throw StatusError{LMS_ERR_COMM, "stream memory operations are not available"};
+  relayout_for_world(world, rank);
+  p2p_disconnect();
+  LMS_CUDA(cudaMemsetAsync(p2p_flags_, 0, 256, stream_));
+  sync();
+  P2PBlob b{};
+  b.magic = kBlobMagic;
+  b.pid = (long long)getpid();
+  b.device = cfg.device;
+  b.rank = rank;
+  b.world = world;
+  b.base = (unsigned long long)reinterpret_cast<uintptr_t>(arena_);
+  b.bytes = arena_bytes_;
+  if (world > 1) LMS_CUDA(cudaIpcGetMemHandle(&b.handle, arena_));
+  std::memset(blob, 0, 128);
+  std::memcpy(blob, &b, sizeof(b));
+}
+
+template <typename T, int D>
+void System<T, D>::p2p_connect(const unsigned char* blobs)
+{
+  P2PBlob mine{};
+  std::memcpy(&mine, blobs + (size_t)rank_ * 128, sizeof(mine));
+  if (mine.magic != kBlobMagic || mine.rank != rank_ || mine.world != world_ ||
+      mine.base != (unsigned long long)reinterpret_cast<uintptr_t>(arena_))
+    throw StatusError{LMS_ERR_STATE, "lms_p2p_connect: this rank's blob is not the one lms_p2p_export produced"};
+  p2p_disconnect();
+  n_peers_ = 0;
+  for (int r = 0; r < world_; ++r) {
+    if (r == rank_) continue;
+    P2PBlob b{};
+    std::memcpy(&b, blobs + (size_t)r * 128, sizeof(b));
+    if (b.magic != kBlobMagic || b.rank != r || b.world != world_ || b.bytes != arena_bytes_)
+      throw StatusError{LMS_ERR_INVALID, "lms_p2p_connect: inconsistent peer blob (same n, T, precision on every rank?)"};
+    char* theirs = nullptr;
+    if (b.pid == (long long)getpid()) {
+      theirs = reinterpret_cast<char*>((uintptr_t)b.base);
+      if (b.device != cfg.device) {
+        int can = 0;
+        LMS_CUDA(cudaDeviceCanAccessPeer(&can, cfg.device, b.device));
+        if (!can) throw StatusError{LMS_ERR_COMM, "peer access between the devices is not possible"};
+        cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) LMS_CUDA(e);
+        cudaGetLastError();
+      }
+    } else {
+      void* mapped = nullptr;
+      LMS_CUDA(cudaIpcOpenMemHandle(&mapped, b.handle, cudaIpcMemLazyEnablePeerAccess));
+      peer_mapping_[n_peers_] = mapped;
+      theirs = static_cast<char*>(mapped);
+    }
+    peer_rank_[n_peers_] = r;
+    peer_delta_[n_peers_] = (long long)(theirs - arena_);
+    ++n_peers_;
+  }
+  p2p_epoch_ = 0;
+  p2p_dirty_ = false;
+  local_ = nullptr;
+  p2p_active_ = world_ > 1;
+  comm_active_ = world_ > 1;
+}
+
+template <typename T, int D>
+void System<T, D>::p2p_disconnect()
+{
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (int k = 0; k < kMaxPeers; ++k) {
+    if (peer_mapping_[k]) cudaIpcCloseMemHandle(peer_mapping_[k]);
+    peer_mapping_[k] = nullptr;
+  }
+  n_peers_ = 0;
+  if (p2p_active_) comm_active_ = false;
+  p2p_active_ = false;
+}
+
+// Announce "everything up to my last launch is in your arena" to every peer, then hold the stream until every
+// peer has announced the same.  Consecutive gathers with no launch in between share one exchange.
+template <typename T, int D>
+void System<T, D>::p2p_exchange()
+{
+  if (!p2p_dirty_) return;
+  p2p_dirty_ = false;
+  const StreamMemOps& ops = stream_mem_ops();
+  ++p2p_epoch_;
+  bool ok = true;
+  for (int k = 0; k < n_peers_; ++k) {
+    unsigned* slot = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(p2p_flags_ + rank_) + peer_delta_[k]);
+    ok = ok && ops.write(stream_, (unsigned long long)reinterpret_cast<uintptr_t>(slot), p2p_epoch_, 0u) == 0;
+  }
+  for (int k = 0; k < n_peers_; ++k)  // CU_STREAM_WAIT_VALUE_GEQ = 0: (int)(*slot - epoch) >= 0, wrap-safe
+    ok = ok && ops.wait(stream_, (unsigned long long)reinterpret_cast<uintptr_t>(p2p_flags_ + peer_rank_[k]),
+                        p2p_epoch_, 0u) == 0;
+  if (!ok) throw StatusError{LMS_ERR_COMM, "stream memory operation failed"};
 }
 
 RowPartition partition_rows(long long n, int world, int rank)

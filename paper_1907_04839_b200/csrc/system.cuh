@@ -87,6 +87,9 @@ class SystemBase {
   virtual void warp_stored(size_t m, const double* pts, double* out) = 0;
   virtual void comm_init(const unsigned char* id, int rank, int world) = 0;
   virtual void join_local_group(LocalGroup* group, int rank) = 0;
+  // peer-push exchange for the row partition (see System::p2p_export)
+  virtual void p2p_export(int rank, int world, unsigned char* blob) = 0;
+  virtual void p2p_connect(const unsigned char* blobs) = 0;
   // population batches: `count` problems listed in ids (all when ids == nullptr); arrays are full-batch sized
   virtual void eval_batch(const double* x, double* grad, double* scalars, int* diverged_step, int count,
                           const int* ids) = 0;
@@ -164,6 +167,8 @@ class System final : public SystemBase {
   void warp_stored(size_t m, const double* pts, double* out) override;
   void comm_init(const unsigned char* id, int rank, int world) override;
   void join_local_group(LocalGroup* group, int rank) override;
+  void p2p_export(int rank, int world, unsigned char* blob) override;
+  void p2p_connect(const unsigned char* blobs) override;
   void eval_batch(const double* x, double* grad, double* scalars, int* diverged_step, int count,
                   const int* ids) override;
   void final_q_batch(double* out) override;
@@ -197,6 +202,9 @@ class System final : public SystemBase {
   void all_gather_doubles(double* buf);
   void gather_inplace(const std::vector<std::pair<char*, size_t>>& buffers);
   void relayout_for_world(int world, int rank);
+  void alloc_exchange_arena();
+  void p2p_exchange();
+  void p2p_disconnect();
 
   cudaStream_t stream_ = nullptr;
   int num_sms_ = 0;
@@ -257,9 +265,32 @@ class System final : public SystemBase {
   bool comm_active_ = false;
   ncclComm_t comm_ = nullptr;
   LocalGroup* local_ = nullptr;
+  // Every buffer a peer may write lives in ONE allocation (traj_, adj_[0..1], d_grad_, h_part_, mm_part_, flags),
+  // so a peer's address of any of them is the local address plus one byte distance per peer.
+  char* arena_ = nullptr;
+  size_t arena_bytes_ = 0;
+  unsigned* p2p_flags_ = nullptr;            // [world]: slot r holds the last epoch rank r announced to this rank
+  bool p2p_active_ = false;
+  bool p2p_dirty_ = false;                   // a pair kernel ran since the last flag exchange
+  unsigned p2p_epoch_ = 0;
+  int n_peers_ = 0;
+  int peer_rank_[kMaxPeers] = {};
+  long long peer_delta_[kMaxPeers] = {};
+  void* peer_mapping_[kMaxPeers] = {};       // cudaIpcOpenMemHandle results (other processes), else nullptr
   int row_tile_begin_(int bm) const;
   int row_tile_end_(int bm) const;
 };
+
+// What lms_p2p_export hands to the peers (LMS_P2P_BLOB_BYTES = 128 in the C ABI).
+struct P2PBlob {
+  unsigned long long magic;
+  long long pid;
+  int device, rank, world, pad;
+  unsigned long long base;   // the exporting process's address of its arena
+  unsigned long long bytes;
+  cudaIpcMemHandle_t handle; // 64 bytes
+};
+static_assert(sizeof(P2PBlob) <= 128, "blob must fit the ABI's buffer");
 
 struct RowPartition {
   long long slice = 0;      // rows per rank (multiple of kRowAlign), identical on every rank

@@ -247,6 +247,19 @@ class HamiltonianSystem:
         buf = (ctypes.c_ubyte * 128).from_buffer_copy(unique_id)
         self._check(self.lib.lms_system_comm_init(self.handle, buf, rank, world))
 
+    def p2p_export(self, rank: int, world: int) -> bytes:
+        """Row partition over the peer-push transport, step 1: lay this handle out as `rank` of `world` and
+        describe its exchange arena (128 bytes to all-gather among the ranks)."""
+        buf = (ctypes.c_ubyte * 128)()
+        self._check(self.lib.lms_p2p_export(self.handle, rank, world, buf))
+        return bytes(buf)
+
+    def p2p_connect(self, blobs):
+        """Step 2: map every peer's arena (`blobs`: the `world` exported blobs in rank order)."""
+        joined = b"".join(blobs)
+        buf = (ctypes.c_ubyte * len(joined)).from_buffer_copy(joined)
+        self._check(self.lib.lms_p2p_connect(self.handle, buf))
+
 
 def gaussian_kernel(r_sq, sigma):
     """gaussian_kernel (shooting.hpp:55-59) in float64; the device evaluates exp(r2 * kernel_scale)."""

@@ -672,3 +672,138 @@ def test_result_document_of_a_registration_reproduces_the_warp(tmp_path):
     s.close()
     assert np.array_equal(tq[-1], doc.warped)  # same kernels, same inputs: bit for bit
     assert doc.avg_after < doc.avg_before
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("world,n", [(2, 1500), (3, 2600), (4, 700), (2, 20000)])
+def test_row_partition_peer_push_in_process(hs, oracle, prec, world, n):
+    """The row partition over the peer-push transport (lms_p2p_*), world > 1 on ONE GPU: every rank is a handle
+    with its own stream and host thread; the kernels' epilogues store each updated row into every rank's arena and
+    only arrival flags are exchanged in stream order.  Same acceptance as the loopback test."""
+    import threading
+
+    from paper_1907_04839_b200 import HamiltonianSystem
+
+    T, lam = 5, 100.0
+    q, p, target, *_ = synth_case(n, 3, 900 + n + world, spread=10.0 if n < 10000 else 60.0)
+    plain = hs(n, 3, prec)
+    plain.bind_registration(q, target, lam, T)
+    want_loss, want_grad = plain.objective(p)
+    want_q = plain.final_q()
+    ranks = [HamiltonianSystem(SIGMA, n, 3, prec, max_timesteps=T) for _ in range(world)]
+    blobs, results, errors = [None] * world, [None] * world, []
+    meet = threading.Barrier(world)
+
+    def run(r):
+        try:
+            s = ranks[r]
+            blobs[r] = s.p2p_export(r, world)
+            meet.wait(timeout=120)  # the application's all-gather of the blobs
+            s.p2p_connect(blobs)
+            s.bind_registration(q, target, lam, T)
+            meet.wait(timeout=120)
+            evals = [s.objective(p) for _ in range(3)]  # later evaluations reuse the arenas the first one wrote
+            results[r] = (evals, s.last_kinetic, s.last_mismatch, s.final_q())
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+            meet.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    tol = 1e-12 if prec == "f64" else 2e-6
+    for r in range(world):
+        evals, kin, mm, fq = results[r]
+        loss, grad = evals[0]
+        assert loss == results[0][0][0][0] and np.array_equal(grad, results[0][0][0][1])  # identical on every rank
+        for again in evals[1:]:
+            assert again[0] == loss and np.array_equal(again[1], grad)                      # and run to run
+        assert loss == pytest.approx(want_loss, rel=tol) and rel_inf(grad, want_grad) <= tol
+        assert kin == pytest.approx(plain.last_kinetic, rel=tol) and mm == pytest.approx(plain.last_mismatch, rel=tol)
+        assert rel_inf(fq, want_q) <= tol
+    for s in ranks:
+        s.close()
+
+
+def _peer_push_worker(rank, world, prec, n, T, lam, seed, to_parent, from_parent):
+    import numpy as np
+
+    from paper_1907_04839_b200 import HamiltonianSystem
+
+    try:
+        rng = np.random.default_rng(seed)
+        q = rng.uniform(-10, 10, (n, 3))
+        p = 0.75 * rng.normal(size=(n, 3))
+        target = q + 0.5 * rng.normal(size=(n, 3))
+        s = HamiltonianSystem(1.5, n, 3, prec, max_timesteps=T)
+        to_parent.put((rank, "blob", s.p2p_export(rank, world)))
+        blobs = from_parent.get(timeout=120)
+        s.p2p_connect(blobs)
+        s.bind_registration(q, target, lam, T)
+        to_parent.put((rank, "bound", None))
+        from_parent.get(timeout=120)
+        first = s.objective(p)
+        second = s.objective(p)
+        to_parent.put((rank, "done", (first, second, s.final_q())))
+        from_parent.get(timeout=120)  # keep the arena mapped until every rank has finished
+        s.close()
+    except Exception as e:  # pragma: no cover
+        to_parent.put((rank, "error", repr(e)))
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_row_partition_peer_push_across_processes(hs, prec):
+    """The production shape of the peer-push transport: one PROCESS per rank, arenas mapped through CUDA IPC
+    (cudaIpcOpenMemHandle), flags through stream memory operations on the mapped memory.  Both ranks share the
+    one GPU of this machine, which exercises everything but the NVLink wires."""
+    import multiprocessing as mp
+
+    world, n, T, lam, seed = 2, 1800, 4, 100.0, 77
+    ctx = mp.get_context("spawn")
+    to_parent = ctx.Queue()
+    inboxes = [ctx.Queue() for _ in range(world)]
+    procs = [ctx.Process(target=_peer_push_worker, args=(r, world, prec, n, T, lam, seed, to_parent, inboxes[r]))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+
+    def collect(tag):
+        got = {}
+        while len(got) < world:
+            rank, kind, payload = to_parent.get(timeout=240)
+            assert kind != "error", payload
+            assert kind == tag, (kind, tag)
+            got[rank] = payload
+        return [got[r] for r in range(world)]
+
+    try:
+        blobs = collect("blob")
+        for box in inboxes:
+            box.put(blobs)
+        collect("bound")
+        for box in inboxes:
+            box.put("go")
+        results = collect("done")
+        for box in inboxes:
+            box.put("bye")
+    finally:
+        for pr in procs:
+            pr.join(timeout=60)
+            if pr.is_alive():
+                pr.kill()
+    rng = np.random.default_rng(seed)
+    q = rng.uniform(-10, 10, (n, 3))
+    p = 0.75 * rng.normal(size=(n, 3))
+    target = q + 0.5 * rng.normal(size=(n, 3))
+    plain = hs(n, 3, prec)
+    plain.bind_registration(q, target, lam, T)
+    want_loss, want_grad = plain.objective(p)
+    tol = 1e-12 if prec == "f64" else 2e-6
+    for (first, second, fq) in results:
+        assert first[0] == results[0][0][0] and np.array_equal(first[1], results[0][0][1])
+        assert second[0] == first[0] and np.array_equal(second[1], first[1])
+        assert first[0] == pytest.approx(want_loss, rel=tol) and rel_inf(first[1], want_grad) <= tol
+        assert rel_inf(fq, plain.final_q()) <= tol
