@@ -315,7 +315,7 @@ def b200_arm(args):
             "n": n, "timesteps": T, "sigma": SIGMA, "lambda": LAMBDA, "units_per_step": "2*T*N^2",
             "template": "Fibonacci sphere, radius 20*sqrt(N/1847) mm (constant landmark density)",
             "l2": "flushed between timed steps (256 MiB write)", "variant": args.variant,
-            "kernel_variant": system.lib.lms_variant_name(0 if prec == "f32" else 1, args.variant).decode(),
+            "kernel_variant": system.lib.lms_system_kernel_names(system.handle).decode(),
         },
         "e2e": {"value": e2e_value, "unit": "pair-evals/s", "h2d_bytes_per_step": int(x0.nbytes),
                 "d2h_bytes_per_step": int(x0.nbytes) + 32, "ms_per_step": wall_host / K},

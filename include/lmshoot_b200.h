@@ -50,7 +50,7 @@ typedef struct lms_config {
   double sigma;      /* Gaussian kernel std, > 0 */
   int max_timesteps; /* capacity of the device-resident trajectory (T + 1 snapshots are stored) */
   int device;        /* CUDA device ordinal */
-  int variant;       /* kernel variant: 0 = library default; see lms_variant_name() */
+  int variant;       /* kernel variant: 0 = library default (by problem size); see lms_variant_name() */
   int reserved;
 } lms_config;
 
@@ -64,6 +64,8 @@ long long lms_last_diverged_point(const lms_system* sys);
 const char* lms_last_error_message(const lms_system* sys);
 const char* lms_status_string(int status);
 const char* lms_variant_name(int precision, int variant);
+/* "<forward kernel> / <adjoint kernel>" this handle launches (variant 0 chooses the shapes by problem size). */
+const char* lms_system_kernel_names(const lms_system* sys);
 
 /* ---- HamiltonianSystem members, one call each (parity-test surface) ---- */
 

@@ -66,6 +66,7 @@ SIGNATURES = {
     "lms_last_error_message": ([c_void_p], c_char_p),
     "lms_status_string": ([c_int], c_char_p),
     "lms_variant_name": ([c_int, c_int], c_char_p),
+    "lms_system_kernel_names": ([c_void_p], c_char_p),
     "lms_hamiltonian": ([c_void_p, _dp, _dp, _dp], c_int),
     "lms_derivatives": ([c_void_p, _dp, _dp, _dp, _dp], c_int),
     "lms_integrate_forward": ([c_void_p, _dp, _dp, c_int, _dp, _dp], c_int),

@@ -70,6 +70,11 @@ const char* lms_variant_name(int precision, int variant)
   return lms::variant_name(precision, variant);
 }
 
+const char* lms_system_kernel_names(const lms_system* sys)
+{
+  return sys && sys->impl ? sys->impl->kernel_names_.c_str() : "";
+}
+
 int lms_system_create(const lms_config* cfg, lms_system** out)
 {
   if (!cfg || !out) return LMS_ERR_INVALID;

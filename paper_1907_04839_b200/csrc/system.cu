@@ -37,7 +37,8 @@ void dev_free(T*& p)
 #define LMS_PICK(T, D, MODE, R, JU, MINB, NAME) make_choice<T, D, MODE, R, JU, MINB>(NAME)
 #define LMS_PICK2(D, MODE, R, JU, MINB, NAME) make_choice<float, D, MODE, R, JU, MINB, true>(NAME)
 
-// fp32, D = 3.  Variant 0 (default) is the packed f32x2 pair the B200 sessions in profiles/ measured fastest:
+// fp32, D = 3.  Variant 0 / 11 (the default below N = 16 000; from there on variant 0 maps to 9, see the System
+// constructor) is the packed f32x2 pair the B200 sessions in profiles/ measured fastest at N = 20 000 and below:
 // forward R=2, 4 columns per LDS.128, 72 registers (7 CTAs/SM); adjoint R=2, 2 columns per load with the column
 // loop unrolled twice, 96 registers (5 CTAs/SM).  1 = the scalar-FFMA kernels (first version, kept as the A/B
 // baseline); 2 = the previous packed default; 3, 4 = other packed shapes; 5 = the default shapes with the column
@@ -162,9 +163,16 @@ System<T, D>::System(const lms_config& c, int batch_count)
   else
     kexp_ = (T)((long double)k_scale * 1.44269504088896340735992468100189214L * (long double)kExpEntries);  // Math<double>::kernel
 
-  k_fwd_ = pick_kernel<T, D, kFwd>(c.variant);
-  k_adj_ = pick_kernel<T, D, kAdj>(c.variant);
+  // Variant 0 picks the shapes by problem size: from N = 16 000 on (single problems, fp32, D = 3) four rows per
+  // thread with column-major tiles -- 2-3.5 % faster there (N = 20 000: 8.05 vs 8.22 ms, N = 100 000: 190.8 vs
+  // 197.6 ms per gradient, same session), but twice the row-tile size, which mid-size and batched problems pay
+  // for in parallelism.  Variant 11 pins the two-row shapes for A/B.
+  int variant = c.variant;
+  if (variant == 0 && sizeof(T) == 4 && D == 3 && batch == 1 && c.n >= 16000) variant = 9;
+  k_fwd_ = pick_kernel<T, D, kFwd>(variant);
+  k_adj_ = pick_kernel<T, D, kAdj>(variant);
   k_vel_ = pick_kernel<T, D, kVel>(c.variant);
+  kernel_names_ = std::string(k_fwd_.name) + " / " + k_adj_.name;
 
   max_t_ = std::max(c.max_timesteps, 1);
   const long long N = (long long)c.n;

@@ -104,6 +104,7 @@ class SystemBase {
   int last_diverged_step = -1;
   long long last_diverged_point = -1;
   std::string last_message;
+  std::string kernel_names_;  // "<forward> / <adjoint>" shapes this handle launches
   double last_eval_ms = 0.0;
   int last_eval_launches = 0;
   bool kernel_timing = false;
