@@ -3,6 +3,7 @@
 
 #include <unistd.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -55,6 +56,9 @@ KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
     case 5: return make_choice<float, 3, kFwd, 2, 4, 7, true, 1, true>("fwd_f32x2_r2_j4_b7_tma");
     case 8: return LMS_PICK2(3, kFwd, 4, 4, 4, "fwd_f32x2_r4_j4_b4");
     case 9: return LMS_PICK2(3, kFwd, 4, 4, 3, "fwd_f32x2_r4_j4_b3");
+    case 12: return LMS_PICK2(3, kFwd, 6, 4, 2, "fwd_f32x2_r6_j4_b2");
+    case 13: return LMS_PICK2(3, kFwd, 8, 2, 2, "fwd_f32x2_r8_j2_b2");
+    case 14: return LMS_PICK2(3, kFwd, 8, 4, 2, "fwd_f32x2_r8_j4_b2");
     default: return LMS_PICK2(3, kFwd, 2, 4, 7, "fwd_f32x2_r2_j4_b7");
   }
 }
@@ -72,6 +76,9 @@ KernelChoice<float> pick_kernel<float, 3, kAdj>(int v)
     case 8: return make_choice<float, 3, kAdj, 4, 1, 4, true, 2, false, true>("adj_f32x2_r4_aos_b4_u2");
     case 9: return make_choice<float, 3, kAdj, 4, 1, 3, true, 4, false, true>("adj_f32x2_r4_aos_b3_u4");
     case 10: return make_choice<float, 3, kAdj, 2, 1, 6, true, 8, false, true>("adj_f32x2_r2_aos_b6_u8");
+    case 12: return make_choice<float, 3, kAdj, 6, 1, 2, true, 2, false, true>("adj_f32x2_r6_aos_b2_u2");
+    case 13: return make_choice<float, 3, kAdj, 8, 1, 2, true, 1, false, true>("adj_f32x2_r8_aos_b2_u1");
+    case 14: return make_choice<float, 3, kAdj, 8, 1, 2, true, 2, false, true>("adj_f32x2_r8_aos_b2_u2");
     default: return make_choice<float, 3, kAdj, 2, 2, 5, true, 2>("adj_f32x2_r2_j2_b5_u2");
   }
 }
@@ -167,16 +174,11 @@ System<T, D>::System(const lms_config& c, int batch_count)
   // thread with column-major tiles -- 2-3.5 % faster there (N = 20 000: 8.05 vs 8.22 ms, N = 100 000: 190.8 vs
   // 197.6 ms per gradient, same session), but twice the row-tile size, which mid-size and batched problems pay
   // for in parallelism.  Variant 11 pins the two-row shapes for A/B.
-  int variant = c.variant;
-  if (variant == 0 && sizeof(T) == 4 && D == 3 && batch == 1 && c.n >= 16000) variant = 9;
-  k_fwd_ = pick_kernel<T, D, kFwd>(variant);
-  k_adj_ = pick_kernel<T, D, kAdj>(variant);
-  k_vel_ = pick_kernel<T, D, kVel>(c.variant);
-  kernel_names_ = std::string(k_fwd_.name) + " / " + k_adj_.name;
+  pick_kernels(/*partitioned=*/false);
 
   max_t_ = std::max(c.max_timesteps, 1);
   const long long N = (long long)c.n;
-  stride_ = std::max<long long>(round_up(N, kRowAlign), kRowAlign);
+  stride_ = std::max<long long>(round_up(N, row_align_), row_align_);
   const size_t plane = (size_t)stride_;
   const size_t B = (size_t)batch;
   bs_traj_ = (long long)(max_t_ + 1) * kState * stride_;
@@ -196,6 +198,33 @@ System<T, D>::System(const lms_config& c, int batch_count)
   LMS_CUDA(cudaMallocHost(&h_scalars_, 4 * B * sizeof(double)));
   part_tiles_ = (int)(stride_ / kThreads);
   alloc_exchange_arena();
+}
+
+// Variant 0 picks the shapes by problem size.  From N = 16 000 on (single problems, fp32, D = 3) four rows per
+// thread pay: every staged column tile and every broadcast LDS serves twice the pairs (N = 20 000: 8.22 -> 8.05 ms,
+// N = 100 000: 197.6 -> 190.8 ms per gradient, same session).  Larger row tiles cost parallelism at mid size and in
+// batches (those keep R = 2, variant 11).  Six or eight rows per thread (variants 12-14) are another 0.8 % faster per
+// pair but lose it again to row-tile quantisation -- a mostly padded last tile costs a full tile: 27 tiles of 768
+// rows for N = 20 000 waste 3.6 %, 40 tiles of 512 waste 2.3 % -- and do not divide the row partition's slices.
+template <typename T, int D>
+void System<T, D>::pick_kernels(bool partitioned)
+{
+  int variant = cfg.variant;
+  if (variant == 0 && sizeof(T) == 4 && D == 3 && batch == 1 && cfg.n >= 16000) variant = 9;
+  k_fwd_ = pick_kernel<T, D, kFwd>(variant);
+  k_adj_ = pick_kernel<T, D, kAdj>(variant);
+  k_vel_ = pick_kernel<T, D, kVel>(cfg.variant);
+  kernel_names_ = std::string(k_fwd_.name) + " / " + k_adj_.name;
+  // planes are padded to a whole number of the largest row tile (and of kRowAlign)
+  long long align = kRowAlign;
+  const int rows_per_thread[3] = {k_fwd_.rows_per_thread, k_adj_.rows_per_thread, k_vel_.rows_per_thread};
+  for (int r : rows_per_thread) {
+    const long long bm = (long long)kThreads * r;
+    align = align / std::__gcd(align, bm) * bm;
+  }
+  if (partitioned && align != kRowAlign)
+    throw StatusError{LMS_ERR_INVALID, "this kernel variant's row tile does not divide the row partition's slices"};
+  row_align_ = align;
 }
 
 // traj_, adj_[0..1], d_grad_, h_part_, mm_part_ and the exchange flags in one allocation (see p2p_export).
@@ -271,6 +300,7 @@ int System<T, D>::row_tile_end_(int bm) const
 {
   const long long slice = stride_ / world_;
   const int live_tiles = ceil_div((long long)cfg.n, bm);
+  if (world_ == 1) return live_tiles;  // row tiles need not divide the padded plane length when nothing is sliced
   return std::min<int>((int)((rank_ + 1) * slice / bm), live_tiles);
 }
 
@@ -286,6 +316,10 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   p.n_j_tiles = ceil_div((long long)cfg.n, kTileJ);
   (void)row_tile0;
   const long long units_per_row = (long long)p.n_j_tiles * kUnitsPerTile;  // work units, see pair_kernel
+  // (Tried: letting the dead warps of a mostly-padded last row tile skip the pair math and giving that tile
+  // proportionally fewer work units.  A CTA's time is set by its busiest warp, not by how many warps work, so the
+  // "cheaper" tile just ran 4x longer per unit: N = 20 000 went from 8.1 to 16-20 ms.  Row tiles that are mostly
+  // padding cost a full tile: 2.3 % of a launch at N = 20 000 with 512-row tiles, 3.6 % with 768.)
   const long long cells = (long long)p.n_row_tiles * units_per_row;
   if (cells <= 0) return p;
   int per_sm = 0;
@@ -909,7 +943,7 @@ void System<T, D>::final_q_batch(double* out)
 template <typename T, int D>
 void System<T, D>::ensure_points(size_t m)
 {
-  const long long need = std::max<long long>(round_up((long long)m, kRowAlign), kRowAlign);
+  const long long need = std::max<long long>(round_up((long long)m, row_align_), row_align_);
   if ((size_t)need > points_cap_) {
     sync();
     dev_free(points_[0]);
@@ -994,7 +1028,8 @@ void System<T, D>::relayout_for_world(int world, int rank)
   sync();
   destroy_graph();
   bound = false;
-  const long long new_stride = partition_rows((long long)cfg.n, world, rank).stride;
+  if (world > 1) pick_kernels(/*partitioned=*/true);
+  const long long new_stride = world > 1 ? partition_rows((long long)cfg.n, world, rank).stride : stride_;
   if (new_stride != stride_) {
     stride_ = new_stride;
     const size_t plane = (size_t)stride_;

@@ -203,6 +203,7 @@ class System final : public SystemBase {
   void all_gather_doubles(double* buf);
   void gather_inplace(const std::vector<std::pair<char*, size_t>>& buffers);
   void relayout_for_world(int world, int rank);
+  void pick_kernels(bool partitioned);
   void alloc_exchange_arena();
   void p2p_exchange();
   void p2p_disconnect();
@@ -214,6 +215,7 @@ class System final : public SystemBase {
   // where the early-scheduled CTAs of the next step compete with the running one.
   bool pdl_ = false;
   long long stride_ = 0;
+  long long row_align_ = kRowAlign;  // plane padding: lcm of kRowAlign and the row tiles in use
   long long bs_traj_ = 0;   // elements between consecutive problems' trajectories
   long long bs_state_ = 0;  // ... between their (alpha,beta) states
   long long bs_vec_ = 0;    // ... between their D-plane vectors (hp0, target, q0)
