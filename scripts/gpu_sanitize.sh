@@ -17,8 +17,24 @@ for prec in ("f32", "f64"):
     q0 = rng.uniform(-6, 6, (5, 300, 3)); t5 = q0 + 0.3 * rng.normal(size=q0.shape)
     b.bind(q0, t5, 10.0, T); b.evaluate((t5 - q0) / T); b.evaluate((t5 - q0) / T, [3, 1]); b.close()
     print(prec, r.loss)
+    # the large-N shapes (four rows per thread, column-major tiles), the device-resident L-BFGS (cooperative two-loop
+    # kernel), and the exchange-arena layout of the peer-push row partition
+    from paper_1907_04839_b200 import ShootingConfig, register_landmarks
+    n = 1100
+    q = rng.uniform(-8, 8, (n, 3)); p = rng.normal(size=(n, 3)); tg = q + 0.3 * rng.normal(size=(n, 3))
+    if prec == "f32":
+        s = HamiltonianSystem(1.5, n, 3, prec, max_timesteps=T, variant=9)
+        print("variant 9", s.compute_gradient(q, p, tg, 10.0, T).loss); s.close()
+    reg = register_landmarks(q, tg, ShootingConfig(sigma=1.5, timesteps=T, lam=100.0, max_iter=4, precision=prec),
+                             device_vectors=True)
+    print("device lbfgs", reg.final_loss)
+    # (the in-process peer-push test is left out: compute-sanitizer serialises kernel launches of the process, so
+    #  a rank's stream-ordered wait for its peer's flag blocks the very launch that would set it)
+    s = HamiltonianSystem(1.5, n, 3, prec, max_timesteps=T)
+    blob = s.p2p_export(0, 1); s.p2p_connect([blob]); s.bind_registration(q, tg, 10.0, T)
+    print("peer-push layout, one rank", s.objective(p)[0]); s.close()
 PY
-timeout 900 compute-sanitizer --tool memcheck --error-exitcode 1 python /tmp/san.py > gpurun_out/sanitizer_memcheck.log 2>&1; echo "memcheck rc=$?"
+timeout 500 compute-sanitizer --tool memcheck --error-exitcode 1 python /tmp/san.py > gpurun_out/sanitizer_memcheck.log 2>&1; echo "memcheck rc=$?"
 tail -4 gpurun_out/sanitizer_memcheck.log
-timeout 900 compute-sanitizer --tool racecheck --error-exitcode 1 python /tmp/san.py > gpurun_out/sanitizer_racecheck.log 2>&1; echo "racecheck rc=$?"
+timeout 500 compute-sanitizer --tool racecheck --error-exitcode 1 python /tmp/san.py > gpurun_out/sanitizer_racecheck.log 2>&1; echo "racecheck rc=$?"
 tail -4 gpurun_out/sanitizer_racecheck.log
