@@ -133,6 +133,35 @@ def test_kernel_variants_agree_with_oracle(hs, oracle, prec, variant):
     assert r.loss == pytest.approx(loss, rel=tol) and rel_inf(r.grad, grad) <= tol
 
 
+@pytest.mark.parametrize("variant", [6, 7, 8, 9, 10, 11, 12, 13, 14])
+@pytest.mark.parametrize("n", [300, 1100, 2300])
+def test_fp32_shape_variants_agree_with_oracle(hs, oracle, variant, n):
+    """Column-major tiles (6, 7, 10), four / six / eight rows per thread (8, 9 = the default from N = 16 000; 12-14),
+    the pinned two-row shapes (11): sizes below, at and above one row tile of every shape (256 .. 1024 rows), with
+    plane lengths that are not multiples of the larger tiles."""
+    q, p, target, *_ = synth_case(n, 3, 700 + variant + n, spread=7.0)
+    s = hs(n, 3, "f32", variant=variant)
+    r = s.compute_gradient(q, p, target, 10.0, 4)
+    loss, kin, mm, grad = oracle.compute_gradient("f32", q, p, target, SIGMA, 10.0, 4)
+    assert r.loss == pytest.approx(loss, rel=1e-5) and rel_inf(r.grad, grad) <= 1e-5
+    again = s.compute_gradient(q, p, target, 10.0, 4)
+    assert np.array_equal(again.grad, r.grad)
+    hq, hp = s.derivatives(q, p)
+    ohq, ohp = oracle.derivatives("f32", q, p, SIGMA)
+    assert rel_inf(hq, ohq) <= 1e-5 and rel_inf(hp, ohp) <= 1e-5
+    alpha, beta = p[::-1].copy(), q[::-1].copy() * 0.1
+    da, db = s.adjoint_step(q, p, alpha, beta)
+    oda, odb = oracle.adjoint_step("f32", q, p, alpha, beta, SIGMA)
+    assert rel_inf(da, oda) <= 1e-5 and rel_inf(db, odb) <= 1e-5
+
+
+def test_default_shapes_switch_with_problem_size(hs):
+    """Variant 0 chooses the kernel shapes by problem size (System::pick_kernels)."""
+    small, large = hs(2000, 3, "f32"), hs(16000, 3, "f32")
+    assert small.lib.lms_system_kernel_names(small.handle) == b"fwd_f32x2_r2_j4_b7 / adj_f32x2_r2_j2_b5_u2"
+    assert large.lib.lms_system_kernel_names(large.handle) == b"fwd_f32x2_r4_j4_b3 / adj_f32x2_r4_aos_b3_u4"
+
+
 def test_known_answers_through_the_abi(hs):
     """SPEC.md:158-216 closed forms, fp64."""
     s1 = hs(1, 3, "f64")
