@@ -86,6 +86,17 @@ class BatchedRegistrations:
                                            div.ctypes.data_as(POINTER(c_int))), self.handle)
         return scalars, grad, div
 
+    def evaluate_ptrs(self, x_ptr: int, grad_ptr: int, scalars_ptr: int, diverged_ptr: int = 0):
+        """The same evaluation of all problems on caller-owned host buffers given as addresses (x, grad: batch x n x
+        dim float64; scalars: batch x 3 float64; diverged: batch int32 or 0) -- e.g. pinned memory, no allocation."""
+        from ctypes import c_void_p, cast
+
+        dp = POINTER(ctypes.c_double)
+        _lib.check(self.lib.lms_batch_eval(self.handle, self.batch, None, cast(c_void_p(x_ptr), dp),
+                                           cast(c_void_p(grad_ptr), dp), cast(c_void_p(scalars_ptr), dp),
+                                           cast(c_void_p(diverged_ptr), POINTER(c_int)) if diverged_ptr else None),
+                   self.handle)
+
     def final_q(self):
         out = np.empty((self.batch, self.n, self.dim))
         _lib.check(self.lib.lms_batch_final_q(self.handle, _ptr(out)), self.handle)
