@@ -116,13 +116,15 @@ KernelChoice<double> pick_kernel<double, 3, kVel>(int)
   return LMS_PICK(double, 3, kVel, 2, 2, 4, "vel_f64_r2_j2");
 }
 template <>
-KernelChoice<float> pick_kernel<float, 2, kFwd>(int)
+KernelChoice<float> pick_kernel<float, 2, kFwd>(int v)
 {
+  if (v == 9) return LMS_PICK2(2, kFwd, 4, 4, 3, "fwd_f32x2_d2_r4_j4_b3");
   return LMS_PICK2(2, kFwd, 2, 4, 7, "fwd_f32x2_d2_r2_j4");
 }
 template <>
-KernelChoice<float> pick_kernel<float, 2, kAdj>(int)
+KernelChoice<float> pick_kernel<float, 2, kAdj>(int v)
 {
+  if (v == 9) return make_choice<float, 2, kAdj, 4, 1, 3, true, 4, false, true>("adj_f32x2_d2_r4_aos_b3_u4");
   return make_choice<float, 2, kAdj, 2, 2, 5, true, 2>("adj_f32x2_d2_r2_j2_u2");
 }
 template <>
@@ -212,7 +214,7 @@ void System<T, D>::pick_kernels(bool partitioned)
   int variant = cfg.variant;
   // (populations: the same shapes once the batch as a whole is that large -- 128 x N = 2000: 10.81 -> 10.49 ms)
   const bool large = batch == 1 ? cfg.n >= 16000 : (cfg.n >= 1024 && (long long)batch * (long long)cfg.n >= 32000);
-  if (variant == 0 && sizeof(T) == 4 && D == 3 && large) variant = 9;
+  if (variant == 0 && sizeof(T) == 4 && large) variant = 9;
   k_fwd_ = pick_kernel<T, D, kFwd>(variant);
   k_adj_ = pick_kernel<T, D, kAdj>(variant);
   k_vel_ = pick_kernel<T, D, kVel>(cfg.variant);

@@ -155,6 +155,16 @@ def test_fp32_shape_variants_agree_with_oracle(hs, oracle, variant, n):
     assert rel_inf(da, oda) <= 1e-5 and rel_inf(db, odb) <= 1e-5
 
 
+@pytest.mark.parametrize("n", [700, 1500])
+def test_two_dimensional_four_row_shapes(hs, oracle, n):
+    """D = 2 with the shapes large problems select (variant 9)."""
+    q, p, target, *_ = synth_case(n, 2, 40 + n, spread=9.0)
+    s = hs(n, 2, "f32", variant=9)
+    r = s.compute_gradient(q, p, target, 10.0, 4)
+    loss, kin, mm, grad = oracle.compute_gradient("f32", q, p, target, SIGMA, 10.0, 4)
+    assert r.loss == pytest.approx(loss, rel=1e-5) and rel_inf(r.grad, grad) <= 1e-5
+
+
 def test_default_shapes_switch_with_problem_size(hs):
     """Variant 0 chooses the kernel shapes by problem size (System::pick_kernels)."""
     small, large = hs(2000, 3, "f32"), hs(16000, 3, "f32")
