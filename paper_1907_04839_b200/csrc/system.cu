@@ -56,6 +56,16 @@ KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
     case 5: return make_choice<float, 3, kFwd, 2, 4, 7, true, 1, true>("fwd_f32x2_r2_j4_b7_tma");
     case 8: return LMS_PICK2(3, kFwd, 4, 4, 4, "fwd_f32x2_r4_j4_b4");
     case 9: return LMS_PICK2(3, kFwd, 4, 4, 3, "fwd_f32x2_r4_j4_b3");
+    case 20: return make_choice<float, 3, kFwd, 4, 2, 3, true, 2>("fwd_f32x2_r4_j2_b3_u2");
+    case 21: return make_choice<float, 3, kFwd, 4, 2, 4, true, 1>("fwd_f32x2_r4_j2_b4");
+    case 22: return make_choice<float, 3, kFwd, 4, 4, 3, true, 2>("fwd_f32x2_r4_j4_b3_u2");
+    case 23: return make_choice<float, 3, kFwd, 4, 1, 3, true, 4>("fwd_f32x2_r4_j1_b3_u4");
+    case 24: return make_choice<float, 3, kFwd, 4, 4, 3, true, 1, true>("fwd_f32x2_r4_j4_b3_tma");
+    case 25: case 30: case 31: case 32: case 33:
+      return make_choice<float, 3, kFwd, 4, 4, 3, true, 2, true>("fwd_f32x2_r4_j4_b3_u2_tma");
+    case 26: return make_choice<float, 3, kFwd, 4, 4, 3, true, 4>("fwd_f32x2_r4_j4_b3_u4");
+    case 27: return make_choice<float, 3, kFwd, 4, 2, 3, true, 4>("fwd_f32x2_r4_j2_b3_u4");
+    case 28: return make_choice<float, 3, kFwd, 4, 4, 2, true, 2>("fwd_f32x2_r4_j4_b2_u2");
     case 12: return LMS_PICK2(3, kFwd, 6, 4, 2, "fwd_f32x2_r6_j4_b2");
     case 13: return LMS_PICK2(3, kFwd, 8, 2, 2, "fwd_f32x2_r8_j2_b2");
     case 14: return LMS_PICK2(3, kFwd, 8, 4, 2, "fwd_f32x2_r8_j4_b2");
@@ -74,8 +84,13 @@ KernelChoice<float> pick_kernel<float, 3, kAdj>(int v)
     case 6: return make_choice<float, 3, kAdj, 2, 1, 5, true, 4, false, true>("adj_f32x2_r2_aos_b5_u4");
     case 7: return make_choice<float, 3, kAdj, 2, 1, 6, true, 4, false, true>("adj_f32x2_r2_aos_b6_u4");
     case 8: return make_choice<float, 3, kAdj, 4, 1, 4, true, 2, false, true>("adj_f32x2_r4_aos_b4_u2");
-    case 9: return make_choice<float, 3, kAdj, 4, 1, 3, true, 4, false, true>("adj_f32x2_r4_aos_b3_u4");
+    case 9: case 20: case 21: case 22: case 23: case 24: case 25: case 26: case 27: case 28:
+      return make_choice<float, 3, kAdj, 4, 1, 3, true, 4, false, true>("adj_f32x2_r4_aos_b3_u4");
     case 10: return make_choice<float, 3, kAdj, 2, 1, 6, true, 8, false, true>("adj_f32x2_r2_aos_b6_u8");
+    case 30: return make_choice<float, 3, kAdj, 4, 2, 3, true, 2, true>("adj_f32x2_r4_j2_b3_u2_tma");
+    case 31: return make_choice<float, 3, kAdj, 4, 4, 3, true, 1, true>("adj_f32x2_r4_j4_b3_tma");
+    case 32: return make_choice<float, 3, kAdj, 4, 2, 3, true, 1, true>("adj_f32x2_r4_j2_b3_tma");
+    case 33: return make_choice<float, 3, kAdj, 4, 1, 3, true, 2, false, true>("adj_f32x2_r4_aos_b3_u2");
     case 12: return make_choice<float, 3, kAdj, 6, 1, 2, true, 2, false, true>("adj_f32x2_r6_aos_b2_u2");
     case 13: return make_choice<float, 3, kAdj, 8, 1, 2, true, 1, false, true>("adj_f32x2_r8_aos_b2_u1");
     case 14: return make_choice<float, 3, kAdj, 8, 1, 2, true, 2, false, true>("adj_f32x2_r8_aos_b2_u2");
@@ -119,12 +134,13 @@ template <>
 KernelChoice<float> pick_kernel<float, 2, kFwd>(int v)
 {
   if (v == 9) return LMS_PICK2(2, kFwd, 4, 4, 3, "fwd_f32x2_d2_r4_j4_b3");
+  if (v == 25) return make_choice<float, 2, kFwd, 4, 4, 3, true, 2, true>("fwd_f32x2_d2_r4_j4_b3_u2_tma");
   return LMS_PICK2(2, kFwd, 2, 4, 7, "fwd_f32x2_d2_r2_j4");
 }
 template <>
 KernelChoice<float> pick_kernel<float, 2, kAdj>(int v)
 {
-  if (v == 9) return make_choice<float, 2, kAdj, 4, 1, 3, true, 4, false, true>("adj_f32x2_d2_r4_aos_b3_u4");
+  if (v == 9 || v == 25) return make_choice<float, 2, kAdj, 4, 1, 3, true, 4, false, true>("adj_f32x2_d2_r4_aos_b3_u4");
   return make_choice<float, 2, kAdj, 2, 2, 5, true, 2>("adj_f32x2_d2_r2_j2_u2");
 }
 template <>
@@ -202,8 +218,9 @@ System<T, D>::System(const lms_config& c, int batch_count)
   alloc_exchange_arena();
 }
 
-// Variant 0 picks the shapes by problem size.  From N = 16 000 on (single problems, fp32, D = 3) four rows per
-// thread pay: every staged column tile and every broadcast LDS serves twice the pairs (N = 20 000: 8.22 -> 8.05 ms,
+// Variant 0 picks the shapes by problem size.  From N = 16 000 on (fp32) four rows per thread pay (variant 25;
+// variant 9 is the same with the forward tiles staged through registers and the column loop not unrolled: forward
+// launch 0.258 -> 0.247 ms at N = 20 000): every staged column tile and every broadcast LDS serves twice the pairs (N = 20 000: 8.22 -> 8.05 ms,
 // N = 100 000: 197.6 -> 190.8 ms per gradient, same session).  Larger row tiles cost parallelism at mid size and in
 // batches (those keep R = 2, variant 11).  Six or eight rows per thread (variants 12-14) are another 0.8 % faster per
 // pair but lose it again to row-tile quantisation -- a mostly padded last tile costs a full tile: 27 tiles of 768
@@ -214,7 +231,7 @@ void System<T, D>::pick_kernels(bool partitioned)
   int variant = cfg.variant;
   // (populations: the same shapes once the batch as a whole is that large -- 128 x N = 2000: 10.81 -> 10.49 ms)
   const bool large = batch == 1 ? cfg.n >= 16000 : (cfg.n >= 1024 && (long long)batch * (long long)cfg.n >= 32000);
-  if (variant == 0 && sizeof(T) == 4 && large) variant = 9;
+  if (variant == 0 && sizeof(T) == 4 && large) variant = 25;
   k_fwd_ = pick_kernel<T, D, kFwd>(variant);
   k_adj_ = pick_kernel<T, D, kAdj>(variant);
   k_vel_ = pick_kernel<T, D, kVel>(cfg.variant);

@@ -133,7 +133,7 @@ def test_kernel_variants_agree_with_oracle(hs, oracle, prec, variant):
     assert r.loss == pytest.approx(loss, rel=tol) and rel_inf(r.grad, grad) <= tol
 
 
-@pytest.mark.parametrize("variant", [6, 7, 8, 9, 10, 11, 12, 13, 14])
+@pytest.mark.parametrize("variant", [6, 7, 8, 9, 10, 11, 12, 13, 14, 20, 22, 25, 31])
 @pytest.mark.parametrize("n", [300, 1100, 2300])
 def test_fp32_shape_variants_agree_with_oracle(hs, oracle, variant, n):
     """Column-major tiles (6, 7, 10), four / six / eight rows per thread (8, 9 = the default from N = 16 000; 12-14),
@@ -157,9 +157,9 @@ def test_fp32_shape_variants_agree_with_oracle(hs, oracle, variant, n):
 
 @pytest.mark.parametrize("n", [700, 1500])
 def test_two_dimensional_four_row_shapes(hs, oracle, n):
-    """D = 2 with the shapes large problems select (variant 9)."""
+    """D = 2 with the shapes large problems select (variant 25)."""
     q, p, target, *_ = synth_case(n, 2, 40 + n, spread=9.0)
-    s = hs(n, 2, "f32", variant=9)
+    s = hs(n, 2, "f32", variant=25)
     r = s.compute_gradient(q, p, target, 10.0, 4)
     loss, kin, mm, grad = oracle.compute_gradient("f32", q, p, target, SIGMA, 10.0, 4)
     assert r.loss == pytest.approx(loss, rel=1e-5) and rel_inf(r.grad, grad) <= 1e-5
@@ -169,7 +169,7 @@ def test_default_shapes_switch_with_problem_size(hs):
     """Variant 0 chooses the kernel shapes by problem size (System::pick_kernels)."""
     small, large = hs(2000, 3, "f32"), hs(16000, 3, "f32")
     assert small.lib.lms_system_kernel_names(small.handle) == b"fwd_f32x2_r2_j4_b7 / adj_f32x2_r2_j2_b5_u2"
-    assert large.lib.lms_system_kernel_names(large.handle) == b"fwd_f32x2_r4_j4_b3 / adj_f32x2_r4_aos_b3_u4"
+    assert large.lib.lms_system_kernel_names(large.handle) == b"fwd_f32x2_r4_j4_b3_u2_tma / adj_f32x2_r4_aos_b3_u4"
 
 
 def test_known_answers_through_the_abi(hs):
