@@ -38,13 +38,20 @@ void dev_free(T*& p)
 #define LMS_PICK(T, D, MODE, R, JU, MINB, NAME) make_choice<T, D, MODE, R, JU, MINB>(NAME)
 #define LMS_PICK2(D, MODE, R, JU, MINB, NAME) make_choice<float, D, MODE, R, JU, MINB, true>(NAME)
 
-// fp32, D = 3.  Variant 0 / 11 (the default below N = 16 000; from there on variant 0 maps to 9, see the System
-// constructor) is the packed f32x2 pair the B200 sessions in profiles/ measured fastest at N = 20 000 and below:
-// forward R=2, 4 columns per LDS.128, 72 registers (7 CTAs/SM); adjoint R=2, 2 columns per load with the column
-// loop unrolled twice, 96 registers (5 CTAs/SM).  1 = the scalar-FFMA kernels (first version, kept as the A/B
-// baseline); 2 = the previous packed default; 3, 4 = other packed shapes; 5 = the default shapes with the column
-// tiles staged by bulk-async copies (TMA, cp.async.bulk + mbarrier) instead of register-staged loads -- measured
-// 1 % slower in fp32 (8.21 vs 8.10 ms) and 1 % faster in fp64, where it is the default.
+// fp32, D = 3.  Variant 0 maps to 25 from N = 16 000 on and to the `default:` shapes below (see pick_kernels):
+//   default   forward R=2, 4 columns per LDS.128, column loop unrolled x2, tiles staged by bulk-async copies (TMA,
+//             cp.async.bulk + mbarrier), 80 registers (6 CTAs/SM); adjoint R=2, 2 columns per load, unrolled x2,
+//             register-staged tiles, 96 registers (5 CTAs/SM)
+//   25        forward R=4, same loop, 168 registers (3 CTAs/SM); adjoint R=4 with column-major tiles (LDS.128)
+// A/B set (bench.py --variant): 1 = scalar-FFMA kernels (first version); 2-5 = earlier packed shapes (5: TMA
+// staging without unrolling); 6, 7, 10 = column-major adjoint tiles at R=2; 8, 9 = R=4 with register-staged forward
+// tiles; 11 = the R=2 default before the forward kernel got TMA + unrolling; 12-14 = R=6 / R=8.
+// Measured per launch at N = 20 000 (one session, ms), forward
+//   R=4: j4 0.2584 | j2_u2 0.2508 | j4_u2 0.2500 | j4_u2_tma 0.2468 | j4_u4 0.2554 | j2_u4 0.2589 | j4_b2_u2 0.2548;
+//   adjoint R=4: aos_u4 0.5536 | aos_u2 0.5660 | j4_tma 0.5558 | j2_u2_tma 0.5633 | j2_tma 0.5661.
+// At N = 10 000 / 5000 (R=2 forward): j4_b7 0.0807 / 0.0332 | j4_b6_u2 0.0847 / 0.0336 | j4_b6_u2_tma 0.0772 / 0.0299 |
+//   j4_b7_u2_tma 0.0825 / 0.0338 | j4_b5_u2_tma 0.0788 / 0.0315; adjoint R=2: j2_b5_u2 0.1595 | + tma 0.1584 |
+//   aos_b5_u4 0.1631 | aos_b6_u4 0.1602.
 template <>
 KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
 {
@@ -56,20 +63,12 @@ KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
     case 5: return make_choice<float, 3, kFwd, 2, 4, 7, true, 1, true>("fwd_f32x2_r2_j4_b7_tma");
     case 8: return LMS_PICK2(3, kFwd, 4, 4, 4, "fwd_f32x2_r4_j4_b4");
     case 9: return LMS_PICK2(3, kFwd, 4, 4, 3, "fwd_f32x2_r4_j4_b3");
-    case 20: return make_choice<float, 3, kFwd, 4, 2, 3, true, 2>("fwd_f32x2_r4_j2_b3_u2");
-    case 21: return make_choice<float, 3, kFwd, 4, 2, 4, true, 1>("fwd_f32x2_r4_j2_b4");
-    case 22: return make_choice<float, 3, kFwd, 4, 4, 3, true, 2>("fwd_f32x2_r4_j4_b3_u2");
-    case 23: return make_choice<float, 3, kFwd, 4, 1, 3, true, 4>("fwd_f32x2_r4_j1_b3_u4");
-    case 24: return make_choice<float, 3, kFwd, 4, 4, 3, true, 1, true>("fwd_f32x2_r4_j4_b3_tma");
-    case 25: case 30: case 31: case 32: case 33:
-      return make_choice<float, 3, kFwd, 4, 4, 3, true, 2, true>("fwd_f32x2_r4_j4_b3_u2_tma");
-    case 26: return make_choice<float, 3, kFwd, 4, 4, 3, true, 4>("fwd_f32x2_r4_j4_b3_u4");
-    case 27: return make_choice<float, 3, kFwd, 4, 2, 3, true, 4>("fwd_f32x2_r4_j2_b3_u4");
-    case 28: return make_choice<float, 3, kFwd, 4, 4, 2, true, 2>("fwd_f32x2_r4_j4_b2_u2");
+    case 11: return LMS_PICK2(3, kFwd, 2, 4, 7, "fwd_f32x2_r2_j4_b7");
     case 12: return LMS_PICK2(3, kFwd, 6, 4, 2, "fwd_f32x2_r6_j4_b2");
     case 13: return LMS_PICK2(3, kFwd, 8, 2, 2, "fwd_f32x2_r8_j2_b2");
     case 14: return LMS_PICK2(3, kFwd, 8, 4, 2, "fwd_f32x2_r8_j4_b2");
-    default: return LMS_PICK2(3, kFwd, 2, 4, 7, "fwd_f32x2_r2_j4_b7");
+    case 25: return make_choice<float, 3, kFwd, 4, 4, 3, true, 2, true>("fwd_f32x2_r4_j4_b3_u2_tma");
+    default: return make_choice<float, 3, kFwd, 2, 4, 6, true, 2, true>("fwd_f32x2_r2_j4_b6_u2_tma");
   }
 }
 template <>
@@ -84,13 +83,8 @@ KernelChoice<float> pick_kernel<float, 3, kAdj>(int v)
     case 6: return make_choice<float, 3, kAdj, 2, 1, 5, true, 4, false, true>("adj_f32x2_r2_aos_b5_u4");
     case 7: return make_choice<float, 3, kAdj, 2, 1, 6, true, 4, false, true>("adj_f32x2_r2_aos_b6_u4");
     case 8: return make_choice<float, 3, kAdj, 4, 1, 4, true, 2, false, true>("adj_f32x2_r4_aos_b4_u2");
-    case 9: case 20: case 21: case 22: case 23: case 24: case 25: case 26: case 27: case 28:
-      return make_choice<float, 3, kAdj, 4, 1, 3, true, 4, false, true>("adj_f32x2_r4_aos_b3_u4");
+    case 9: case 25: return make_choice<float, 3, kAdj, 4, 1, 3, true, 4, false, true>("adj_f32x2_r4_aos_b3_u4");
     case 10: return make_choice<float, 3, kAdj, 2, 1, 6, true, 8, false, true>("adj_f32x2_r2_aos_b6_u8");
-    case 30: return make_choice<float, 3, kAdj, 4, 2, 3, true, 2, true>("adj_f32x2_r4_j2_b3_u2_tma");
-    case 31: return make_choice<float, 3, kAdj, 4, 4, 3, true, 1, true>("adj_f32x2_r4_j4_b3_tma");
-    case 32: return make_choice<float, 3, kAdj, 4, 2, 3, true, 1, true>("adj_f32x2_r4_j2_b3_tma");
-    case 33: return make_choice<float, 3, kAdj, 4, 1, 3, true, 2, false, true>("adj_f32x2_r4_aos_b3_u2");
     case 12: return make_choice<float, 3, kAdj, 6, 1, 2, true, 2, false, true>("adj_f32x2_r6_aos_b2_u2");
     case 13: return make_choice<float, 3, kAdj, 8, 1, 2, true, 1, false, true>("adj_f32x2_r8_aos_b2_u1");
     case 14: return make_choice<float, 3, kAdj, 8, 1, 2, true, 2, false, true>("adj_f32x2_r8_aos_b2_u2");
@@ -135,7 +129,8 @@ KernelChoice<float> pick_kernel<float, 2, kFwd>(int v)
 {
   if (v == 9) return LMS_PICK2(2, kFwd, 4, 4, 3, "fwd_f32x2_d2_r4_j4_b3");
   if (v == 25) return make_choice<float, 2, kFwd, 4, 4, 3, true, 2, true>("fwd_f32x2_d2_r4_j4_b3_u2_tma");
-  return LMS_PICK2(2, kFwd, 2, 4, 7, "fwd_f32x2_d2_r2_j4");
+  if (v == 11) return LMS_PICK2(2, kFwd, 2, 4, 7, "fwd_f32x2_d2_r2_j4");
+  return make_choice<float, 2, kFwd, 2, 4, 6, true, 2, true>("fwd_f32x2_d2_r2_j4_b6_u2_tma");
 }
 template <>
 KernelChoice<float> pick_kernel<float, 2, kAdj>(int v)

@@ -5,6 +5,6 @@ mkdir -p gpurun_out
 TAG=$1; shift
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 3 --no-extras "$@" > gpurun_out/ncu_launch_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 38 -c 4 -f -o gpurun_out/prof_$TAG \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 49 -c 2 -f -o gpurun_out/prof_$TAG \
     python bench.py --steps 1 --warmup 3 --no-extras "$@" > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -2 gpurun_out/ncu_full_$TAG.log | cut -c1-300

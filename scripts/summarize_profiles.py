@@ -87,9 +87,9 @@ keep = [
     "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
 ]
 with open(f"profiles/{tag}_ncu_full.md", "w") as f:
-    f.write(f"# {tag}: `ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 38 -c 4` "
+    f.write(f"# {tag}: `ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 49 -c 2` "
             f"on `python bench.py --steps 1 --warmup 3 --no-extras {bench_args}`\n\n")
-    f.write("Two forward and two adjoint pair-kernel launches of a warm-up evaluation (N = 20 000, T = 10).\n\n")
+    f.write("The last forward and the first adjoint pair-kernel launch of a warm-up evaluation (N = 20 000, T = 10).\n\n")
     f.write("| metric | unit | " + " | ".join(short(d[ix["Kernel Name"]]) for d in data) + " |\n")
     f.write("|---|---|" + "---:|" * len(data) + "\n")
     for k in keep:

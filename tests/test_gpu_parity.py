@@ -133,7 +133,7 @@ def test_kernel_variants_agree_with_oracle(hs, oracle, prec, variant):
     assert r.loss == pytest.approx(loss, rel=tol) and rel_inf(r.grad, grad) <= tol
 
 
-@pytest.mark.parametrize("variant", [6, 7, 8, 9, 10, 11, 12, 13, 14, 20, 22, 25, 31])
+@pytest.mark.parametrize("variant", [0, 6, 7, 8, 9, 10, 11, 12, 13, 14, 25])
 @pytest.mark.parametrize("n", [300, 1100, 2300])
 def test_fp32_shape_variants_agree_with_oracle(hs, oracle, variant, n):
     """Column-major tiles (6, 7, 10), four / six / eight rows per thread (8, 9 = the default from N = 16 000; 12-14),
@@ -168,7 +168,7 @@ def test_two_dimensional_four_row_shapes(hs, oracle, n):
 def test_default_shapes_switch_with_problem_size(hs):
     """Variant 0 chooses the kernel shapes by problem size (System::pick_kernels)."""
     small, large = hs(2000, 3, "f32"), hs(16000, 3, "f32")
-    assert small.lib.lms_system_kernel_names(small.handle) == b"fwd_f32x2_r2_j4_b7 / adj_f32x2_r2_j2_b5_u2"
+    assert small.lib.lms_system_kernel_names(small.handle) == b"fwd_f32x2_r2_j4_b6_u2_tma / adj_f32x2_r2_j2_b5_u2"
     assert large.lib.lms_system_kernel_names(large.handle) == b"fwd_f32x2_r4_j4_b3_u2_tma / adj_f32x2_r4_aos_b3_u4"
 
 
