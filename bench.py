@@ -364,6 +364,10 @@ def b200_arm(args):
             "hbm": {"algorithmic_bytes_per_launch": bytes_per_launch,
                     "achieved_gbs": bytes_per_launch / (adj_ms * 1e-3) / 1e9, "peak_gbs": peaks.get("hbm_gbs")},
             "kernel_share_of_step": (fwd_ms + adj_ms) * T / (dev_ms / K),
+            # the same launch in flop terms (FMA = 2 flop; 69 flop per adjoint pair, 28 per forward
+            # pair) against the all-FMA peak of the pipe: lower than `frac` because only ~60 % of the slots are FMAs
+            "flops": {"achieved_tflops": (69 if prec == "f32" else 69) * pairs_per_launch / (adj_ms * 1e-3) / 1e12,
+                      "peak_tflops": 2 * peak_slots / 1e12, "flop_per_pair": 69},
         }
         ub = ffma_peak_lanes()
         if ub and prec == "f32" and "ffma" in ub:
