@@ -366,7 +366,7 @@ def b200_arm(args):
             "kernel_share_of_step": (fwd_ms + adj_ms) * T / (dev_ms / K),
             # the same launch in flop terms (FMA = 2 flop; 69 flop per adjoint pair, 28 per forward
             # pair) against the all-FMA peak of the pipe: lower than `frac` because only ~60 % of the slots are FMAs
-            "flops": {"achieved_tflops": (69 if prec == "f32" else 69) * pairs_per_launch / (adj_ms * 1e-3) / 1e12,
+            "flops": {"achieved_tflops": 69 * pairs_per_launch / (adj_ms * 1e-3) / 1e12,
                       "peak_tflops": 2 * peak_slots / 1e12, "flop_per_pair": 69},
         }
         ub = ffma_peak_lanes()
