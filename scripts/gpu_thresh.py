@@ -9,7 +9,7 @@ for n in [int(a) for a in sys.argv[1:]]:
     target = q0 + 0.5 * rng_normals(1, n * 3).reshape(n, 3)
     x0 = np.ascontiguousarray(((target - q0) / T).ravel())
     row = []
-    for v in (11, 9):
+    for v in (0, 25):
         s = HamiltonianSystem(1.5, n, 3, "f32", max_timesteps=T, variant=v)
         s.bind_registration(q0, target, 5e5, T)
         ms = []
