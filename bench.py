@@ -178,18 +178,24 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    T = args.timesteps or 10
-    n = 20000 if args.gpus == 1 else 200000  # the workload our own arm measures at this --gpus
+    rows_mode = args.gpus > 1 and args.mode == "rows"  # the workload our own arm measures at this --gpus
+    T = args.timesteps or (20 if rows_mode else 10)
+    n = 200000 if rows_mode else 20000
     n_sample = args.n or CPU_SAMPLE_N
     res = cpu_reference_run(n_sample, T, args.precision, max(args.steps, 1), max(args.warmup, 0))
     line = {
         "impl": "reference", "metric": "pair_kernel_evals_per_sec_per_gradient", "value": res["value"],
         "unit": "pair-evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": res["sec_per_gradient"] * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": res["sec_per_gradient"] * 1e3, "higher_is_better": True,
+        "scaling": "strong" if rows_mode else "weak",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
         # our arm's workload; every step times the reference on a bounded sample of it (same generator, same
         # landmark density, same T, sigma, lambda), throughput counted in the same unit
-        "config": {"workload": f"single registration N={n}, T={T}, one fwd+bwd gradient per step", "n": n,
+        "config": {"workload": (f"single registration N={n}, T={T}, row-partitioned over {args.gpus} GPUs, per-step "
+                                + ("NCCL all-gather" if args.exchange == "nccl" else "peer-push exchange (P2P stores + flags)")
+                                if rows_mode else
+                                f"single registration N={n}, T={T}, one fwd+bwd gradient per step"
+                                + (f", {args.gpus} independent replicas" if args.gpus > 1 else "")), "n": n,
                    "timesteps": T, "sigma": SIGMA, "lambda": LAMBDA, "units_per_step": "2*T*N^2",
                    "template": "Fibonacci sphere, radius 20*sqrt(N/1847) mm (constant landmark density)",
                    "sample": res["sample"], "n_sample": n_sample},
