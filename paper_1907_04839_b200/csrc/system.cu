@@ -559,7 +559,7 @@ void System<T, D>::hamiltonian(const double* q, const double* p, double* out)
   a.epi = kEpiRaw | kEpiFirstStep;
   launch<kFwd>(k_fwd_, a, plan);
   // partials are indexed in 128-row units (rt * R), zero where no tile starts
-  finalize_scalars<0><<<1, 32, 0, stream_>>>(h_part_, mm_part_, part_tiles_, 0.0, d_scalars_);
+  finalize_scalars<0><<<1, 128, 0, stream_>>>(h_part_, mm_part_, part_tiles_, 0.0, d_scalars_);
   LMS_CUDA(cudaGetLastError());
   LMS_CUDA(cudaMemcpyAsync(h_scalars_, d_scalars_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   sync();
@@ -773,7 +773,7 @@ void System<T, D>::enqueue_eval(bool timed, int count, const int* d_ids)
     all_gather_doubles(h_part_);
     all_gather_doubles(mm_part_);
   }
-  finalize_scalars<0><<<count, 32, 0, stream_>>>(h_part_, mm_part_, part_tiles_, lambda, d_scalars_, d_ids);
+  finalize_scalars<0><<<count, 128, 0, stream_>>>(h_part_, mm_part_, part_tiles_, lambda, d_scalars_, d_ids);
   LMS_CUDA(cudaGetLastError());
   ++last_eval_launches;
   // discrete adjoint sweep t = T-1 .. 0 (shooting.hpp:300-307), final gradient fused into the t = 0 launch
