@@ -22,6 +22,7 @@
 // are bitwise reproducible run to run (reduction.hpp:38-40 promises the same of the CPU backends).
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -37,6 +38,7 @@ constexpr int kThreads = 128;  // threads per CTA
 constexpr int kTileJ = 128;    // columns staged per shared-memory tile
 constexpr int kUnitJ = 8;      // stream-K work unit: kUnitJ columns of one row tile
 constexpr int kUnitsPerTile = kTileJ / kUnitJ;
+constexpr int kClusterSize = 16;  // CTAs per row tile in the cluster-combine kernels (non-portable cluster size)
 constexpr int kMaxPeers = 7;   // row partition: up to 8 GPUs of one NVSwitch domain
 
 enum Mode : int { kFwd = 0, kAdj = 1, kVel = 2 };
@@ -468,10 +470,16 @@ __device__ __forceinline__ double block_sum(double v, double* scratch)
 // the register-staged path (every thread transposes its own column with 16-byte stores), so one column
 // costs NC/4 LDS.128 with only NC registers of column data live (the plane layout needs JU = 4 columns,
 // 4 NC registers, for the same load count).
+// CLUSTER: small problems.  The launch is kClusterSize CTAs per row tile, each with an equal share of the columns,
+// started as one thread-block cluster; the tile's partial sums meet in distributed shared memory (every CTA parks
+// its sums in its own tile buffers, rank 0 adds the kClusterSize copies in ascending column order and runs the
+// epilogue) instead of going through global slots, a fence, an arrival counter and L2 round trips.
 template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false,
-          bool AOS = false>
+          bool AOS = false, bool CLUSTER = false>
 __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> a)
 {
+  static_assert(!CLUSTER || 2 * Shape<MODE, D>::kColComps * kTileJ >= Shape<MODE, D>::kAcc * kThreads * R,
+                "the tile buffers must hold one set of partial sums");
   static_assert(!PACKED || (sizeof(T) == 4 && R % 2 == 0), "the packed path is fp32 with an even row count");
   static_assert(!AOS || (sizeof(T) == 4 && JU == 1 && !BULK && Shape<MODE, D>::kColComps % 4 == 0),
                 "column-major tiles: fp32, one column per step, register-staged, 16-byte multiples");
@@ -702,7 +710,34 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     const long long cta_first = ((cell_lo + 1) * G - 1) / cells;
     const long long cta_last = ((cell_hi + 1) * G - 1) / cells;
     bool do_epilogue = true;
-    if (cta_first != cta_last) {
+    if constexpr (CLUSTER) {
+      namespace cg = cooperative_groups;
+      cg::cluster_group cluster = cg::this_cluster();
+      // every sweep of this CTA is over (one range per CTA in this mode): the tile buffers are free
+      T* mine = reinterpret_cast<T*>(&tile[0][0][0]);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int k = 0; k < NA; ++k) mine[k * BM + r * kThreads + tid] = acc[r][k];
+      cluster.sync();
+      do_epilogue = cluster.block_rank() == 0;
+      if (do_epilogue) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int k = 0; k < NA; ++k) acc[r][k] = T(0);
+        // cluster rank = column segment: ascending ranks = ascending columns
+#pragma unroll 4
+        for (int ord = 0; ord < kClusterSize; ++ord) {
+          const T* theirs = cluster.map_shared_rank(mine, ord);
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int k = 0; k < NA; ++k) acc[r][k] += theirs[k * BM + r * kThreads + tid];
+        }
+      }
+      cluster.sync();  // nobody's shared memory goes away before rank 0 has read it
+    } else if (cta_first != cta_last) {
       // slot of segment `ord` of row tile rt_local: rt_local * max_seg + ord (ord = CTA index - first CTA)
       const long long slot = rt_local * a.max_seg + ((long long)blockIdx.x - cta_first);
       T* mine = a.partials + slot * (NA * BM);

@@ -120,16 +120,18 @@ class SystemBase {
 template <typename T>
 struct KernelChoice {
   void (*fn)(PairArgs<T>) = nullptr;
+  void (*fn_cluster)(PairArgs<T>) = nullptr;  // same shape with the cluster combine (small problems), or null
   int rows_per_thread = 0;
   const char* name = "";
 };
 
 template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false,
-          bool AOS = false>
+          bool AOS = false, bool WITH_CLUSTER = false>
 KernelChoice<T> make_choice(const char* name)
 {
   KernelChoice<T> c;
   c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS>;
+  if constexpr (WITH_CLUSTER) c.fn_cluster = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, true>;
   c.rows_per_thread = R;
   c.name = name;
   return c;
@@ -145,6 +147,7 @@ struct LaunchPlan {
   int n_row_tiles = 0;
   int n_j_tiles = 0;
   int tiles_per_problem = 1;
+  bool cluster = false;  // launch fn_cluster as clusters of kClusterSize CTAs, one cluster per row tile
   int bm = 0;
   size_t partial_elems = 0;
 };
@@ -214,6 +217,10 @@ class System final : public SystemBase {
   // evaluation graph: no gain at N >= 10 000 (8.088 vs 8.085 ms) and a loss at N = 2000..5000 (0.28 vs 0.25 ms),
   // where the early-scheduled CTAs of the next step compete with the running one.
   bool pdl_ = false;
+  // cluster combine for small single problems (pair_kernel<..., CLUSTER>): opt-in with LMS_CLUSTER=1.  It is worth
+  // 8-12 % below N = 1500 in fp32 (plan_for), but it changes the summation order of those sizes (the partitioned and
+  // unpartitioned paths then no longer agree bit for bit) and must stay off for several ranks on one GPU.
+  bool cluster_combine_ = false;
   long long stride_ = 0;
   long long row_align_ = kRowAlign;  // plane padding: lcm of kRowAlign and the row tiles in use
   long long bs_traj_ = 0;   // elements between consecutive problems' trajectories
