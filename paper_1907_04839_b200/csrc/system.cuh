@@ -140,6 +140,16 @@ KernelChoice<T> make_choice(const char* name)
 // variant 0 is the library default; the others exist so one GPU session can A/B them.
 template <typename T, int D, int MODE>
 KernelChoice<T> pick_kernel(int variant);
+// specialised in system_{f32,f64}_d{2,3}.cu
+#define LMS_DECLARE_PICKS(T, D)                              \
+  template <> KernelChoice<T> pick_kernel<T, D, kFwd>(int);  \
+  template <> KernelChoice<T> pick_kernel<T, D, kAdj>(int);  \
+  template <> KernelChoice<T> pick_kernel<T, D, kVel>(int);
+LMS_DECLARE_PICKS(float, 3)
+LMS_DECLARE_PICKS(double, 3)
+LMS_DECLARE_PICKS(float, 2)
+LMS_DECLARE_PICKS(double, 2)
+#undef LMS_DECLARE_PICKS
 
 struct LaunchPlan {
   int grid = 0;

@@ -122,7 +122,7 @@ def test_two_dimensional_landmarks(hs, oracle, prec):
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [1, 5])
 def test_kernel_variants_agree_with_oracle(hs, oracle, prec, variant):
     tol = TOL[prec]
     n = 700
@@ -133,12 +133,12 @@ def test_kernel_variants_agree_with_oracle(hs, oracle, prec, variant):
     assert r.loss == pytest.approx(loss, rel=tol) and rel_inf(r.grad, grad) <= tol
 
 
-@pytest.mark.parametrize("variant", [0, 6, 7, 8, 9, 10, 11, 12, 13, 14, 25])
+@pytest.mark.parametrize("variant", [0, 11, 25])
 @pytest.mark.parametrize("n", [300, 1100, 2300])
 def test_fp32_shape_variants_agree_with_oracle(hs, oracle, variant, n):
-    """Column-major tiles (6, 7, 10), four / six / eight rows per thread (8, 9 = the default from N = 16 000; 12-14),
-    the pinned two-row shapes (11): sizes below, at and above one row tile of every shape (256 .. 1024 rows), with
-    plane lengths that are not multiples of the larger tiles."""
+    """The default shapes (0), the pinned two-row shapes (11) and four rows per thread with column-major adjoint
+    tiles (25 = the default from N = 16 000): sizes below, at and above one row tile of every shape (256 / 512 rows),
+    with plane lengths that are not multiples of the larger tile."""
     q, p, target, *_ = synth_case(n, 3, 700 + variant + n, spread=7.0)
     s = hs(n, 3, "f32", variant=variant)
     r = s.compute_gradient(q, p, target, 10.0, 4)
