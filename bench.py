@@ -30,9 +30,17 @@ if ROOT not in sys.path:
 SIGMA, LAMBDA = 1.5, 5e5  # shooting.hpp:26-28
 FWD_SLOTS, ADJ_SLOTS = 18, 43  # FP32 lane-instructions per pair, SURVEY.md §8d (fp64: 35 / 60)
 FWD_SLOTS_F64, ADJ_SLOTS_F64 = 35, 60
-# CPU arm: the reference's compute_gradient on a sample of the workload at the same landmark density; N = 6000 is
-# (2T+2) * 3.6e7 pair evaluations = about 1 s per gradient on 16 host threads, 15-20 core-seconds of CPU work
+# lane-instructions the kernels actually execute per pair, MUFU/exp included (profiles/r2_sass_*.md)
+FWD_EXEC, ADJ_EXEC = 18, 40
+FWD_EXEC_F64, ADJ_EXEC_F64 = 28, 50
+# CPU legs.  `--impl reference` runs the reference's compute_gradient on the SAME configuration our arm prints
+# (N = 20 000, T = 10: (2T+2) N^2 = 8.8e9 pair evaluations, ~10 s per gradient on 16 host threads) and caps the number
+# of timed steps by wall clock instead of shrinking N; only configs[2] (N = 200 000, T = 20: ~30 min per gradient)
+# is sampled, and then `config.n` carries the N actually run.  The in-line `cpu_baseline` of the B200 arm is a
+# bounded sample (N = 6000, same generator and density, ~1 s per gradient).
 CPU_SAMPLE_N = 6000
+REF_ROWS_SAMPLE_N = 20000      # reference arm, rows mode: the sample of the N = 200 000 workload
+REF_BUDGET_S = 90.0            # reference arm: wall-clock budget for the timed steps
 
 
 def parse_args():
@@ -51,7 +59,65 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=0, help="population mode: B registrations of --n landmarks per GPU")
     ap.add_argument("--no-extras", action="store_true", help="skip fp64, L-BFGS and cpu_baseline legs")
     ap.add_argument("--lbfgs-iters", type=int, default=30)
+    ap.add_argument("--fixed-extent", action="store_true",
+                    help="template on the fixed 40 mm sphere (synth.hpp:20) instead of constant landmark density")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="start the ranks exactly as a measurement would, report who showed up, measure nothing")
     return ap.parse_args()
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` outside torchrun: start the N ranks ourselves, the way the driver does
+    (python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 ...)."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def init_ranks():
+    """Rank / device / process group from the torchrun environment.  More ranks than visible GPUs (a one-GPU box
+    running a two-rank check) share devices round-robin: the control plane then runs over gloo and the data path over
+    the peer-push exchange (CUDA IPC), because NCCL refuses two ranks on one device."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    device = local_rank % ndev if ndev else -1
+    oversub = ndev > 0 and world > ndev
+    backend = "nccl" if (ndev and not oversub) else "gloo"
+    if ndev:
+        torch.cuda.set_device(device)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, device, oversub, backend
+
+
+def launch_check(args):
+    import torch.distributed as dist
+
+    world, rank, device, oversub, backend = init_ranks()
+    seen = [None] * world
+    if world > 1:
+        dist.all_gather_object(seen, {"rank": rank, "pid": os.getpid(), "device": device})
+        dist.destroy_process_group()
+    else:
+        seen = [{"rank": rank, "pid": os.getpid(), "device": device}]
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "requested": args.gpus, "backend": backend,
+                          "oversubscribed": oversub, "ranks": seen}), flush=True)
 
 
 # ---- clocks -----------------------------------------------------------------------------------------
@@ -136,41 +202,60 @@ def ffma_peak_lanes():
 
 
 # ---- the reference arm ------------------------------------------------------------------------------------
-def cpu_reference_run(n_sample, timesteps, precision, steps, warmup):
-    """Times the reference's compute_gradient (shooting.hpp:277-315) on all host threads."""
+def template_label(fixed_extent):
+    return ("Fibonacci sphere, fixed 40 mm diameter (synth.hpp:20)" if fixed_extent else
+            "Fibonacci sphere, radius 20*sqrt(N/1847) mm (constant landmark density)")
+
+
+def cpu_workload(n, timesteps, fixed_extent, cpu, oracle):
+    """The GPU arm's generator, host-only: Fibonacci sphere, Rng(0) momenta, target = fp64 flow of the template
+    (synth.hpp:40-43), x0 = (target - q0)/T (registration.cpp:47-52)."""
     import numpy as np
 
+    golden = np.pi * (3.0 - np.sqrt(5.0))
+    i = np.arange(n, dtype=np.float64)
+    z = 1.0 - 2.0 * (i + 0.5) / n
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    radius = 20.0 if fixed_extent else 20.0 * np.sqrt(n / 1847.0)
+    q0 = np.stack([radius * r * np.cos(golden * i), radius * r * np.sin(golden * i), radius * z], axis=1)
+    p_true = (0.75 * oracle.rng_normals(0, n * 3)).reshape(n, 3)
+    target = cpu.integrate_forward("f64", q0, p_true, SIGMA, timesteps)[0][-1]
+    return q0, target, (target - q0) / timesteps
+
+
+def cpu_reference_run(n_run, timesteps, precision, steps, warmup, fixed_extent=False, budget_s=None, n_workload=None):
+    """Times the reference's compute_gradient (shooting.hpp:277-315) on all host threads.  With a wall-clock budget
+    the first gradient is the warm-up and sets how many timed steps fit (at least 2, at most `steps`)."""
     from oracle import load_oracle, load_reference, reference_available
 
     kind = "reference" if reference_available() else "port"
     cpu = load_reference() if kind == "reference" else load_oracle()
     cores = cpu.hardware_threads()
-    oracle = load_oracle()
-    # same generator as the GPU arm, host-only: Fibonacci sphere at the same point density, Rng(0) momenta,
-    # target = fp64 flow of the template (synth.hpp:40-43)
-    golden = np.pi * (3.0 - np.sqrt(5.0))
-    i = np.arange(n_sample, dtype=np.float64)
-    z = 1.0 - 2.0 * (i + 0.5) / n_sample
-    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
-    radius = 20.0 * np.sqrt(n_sample / 1847.0)  # constant landmark density (synth.hpp:19-20)
-    q0 = np.stack([radius * r * np.cos(golden * i), radius * r * np.sin(golden * i), radius * z], axis=1)
-    p_true = (0.75 * oracle.rng_normals(0, n_sample * 3)).reshape(n_sample, 3)
-    target = cpu.integrate_forward("f64", q0, p_true, SIGMA, timesteps)[0][-1]
-    x0 = (target - q0) / timesteps
-    times = []
-    for s in range(warmup + steps):
+    q0, target, x0 = cpu_workload(n_run, timesteps, fixed_extent, cpu, load_oracle())
+
+    def one():
         t0 = time.perf_counter()
         cpu.compute_gradient(precision, q0, x0, target, SIGMA, LAMBDA, timesteps)
-        dt = time.perf_counter() - t0
-        if s >= warmup:
-            times.append(dt)
+        return time.perf_counter() - t0
+
+    first = one()
+    if budget_s is not None and first * (steps + warmup) > budget_s:
+        warmup_run, steps_run = 1, max(2, min(steps, int(budget_s / first)))
+    else:
+        warmup_run, steps_run = max(warmup, 1), steps
+    for _ in range(warmup_run - 1):
+        one()
+    times = [one() for _ in range(steps_run)]
     sec = sum(times) / len(times)
-    units = 2.0 * timesteps * n_sample * n_sample
+    units = 2.0 * timesteps * n_run * n_run
+    full = n_workload is None or n_workload == n_run
     return {
         "value": units / sec, "sec_per_gradient": sec, "cores": cores, "kind": kind,
-        "sample": f"full compute_gradient on N={n_sample} (same generator and density as the N=20000 workload), "
-                  f"T={timesteps}, {precision}, blocked_tree/256, {cores} threads; units counted as 2*T*N^2",
-        "n_sample": n_sample,
+        "steps_run": steps_run, "warmup_run": warmup_run, "n_run": n_run,
+        "sample": (f"{'the full workload' if full else f'a sample of the N={n_workload} workload'}: compute_gradient at "
+                   f"N={n_run}, T={timesteps}, {precision}, blocked_tree/256, {cores} threads, {steps_run} timed "
+                   f"gradients after {warmup_run} warm-up; same generator, "
+                   f"{'fixed 40 mm sphere' if fixed_extent else 'same landmark density'}; units counted as 2*T*N^2"),
     }
 
 
@@ -180,49 +265,77 @@ def reference_arm(args):
         return
     rows_mode = args.gpus > 1 and args.mode == "rows"  # the workload our own arm measures at this --gpus
     T = args.timesteps or (20 if rows_mode else 10)
-    n = 200000 if rows_mode else 20000
-    n_sample = args.n or CPU_SAMPLE_N
-    res = cpu_reference_run(n_sample, T, args.precision, max(args.steps, 1), max(args.warmup, 0))
+    n_workload = args.n or (200000 if rows_mode else 20000)
+    # configs[1] runs in full; one N = 200 000, T = 20 gradient is ~30 min of 16 host threads, so configs[2] is
+    # sampled at N = 20 000 (same density, same T) and config.n says so
+    n_run = min(n_workload, REF_ROWS_SAMPLE_N) if rows_mode else n_workload
+    res = cpu_reference_run(n_run, T, args.precision, max(args.steps, 1), max(args.warmup, 0),
+                            fixed_extent=args.fixed_extent, budget_s=REF_BUDGET_S, n_workload=n_workload)
     line = {
         "impl": "reference", "metric": "pair_kernel_evals_per_sec_per_gradient", "value": res["value"],
-        "unit": "pair-evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "unit": "pair-evals/s", "n_gpus": args.gpus, "steps": res["steps_run"], "warmup": res["warmup_run"],
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
         "ms_per_step": res["sec_per_gradient"] * 1e3, "higher_is_better": True,
         "scaling": "strong" if rows_mode else "weak",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-        # our arm's workload; every step times the reference on a bounded sample of it (same generator, same
-        # landmark density, same T, sigma, lambda), throughput counted in the same unit
-        "config": {"workload": (f"single registration N={n}, T={T}, row-partitioned over {args.gpus} GPUs, per-step "
-                                + ("NCCL all-gather" if args.exchange == "nccl" else "peer-push exchange (P2P stores + flags)")
+        "config": {"workload": (f"single registration N={n_workload}, T={T}, row-partitioned over {args.gpus} GPUs"
                                 if rows_mode else
-                                f"single registration N={n}, T={T}, one fwd+bwd gradient per step"
-                                + (f", {args.gpus} independent replicas" if args.gpus > 1 else "")), "n": n,
+                                f"single registration N={n_workload}, T={T}, one fwd+bwd gradient per step"
+                                + (f", {args.gpus} independent replicas" if args.gpus > 1 else "")),
+                   "n": n_run, "n_workload": n_workload,
                    "timesteps": T, "sigma": SIGMA, "lambda": LAMBDA, "units_per_step": "2*T*N^2",
-                   "template": "Fibonacci sphere, radius 20*sqrt(N/1847) mm (constant landmark density)",
-                   "sample": res["sample"], "n_sample": n_sample},
+                   "template": template_label(args.fixed_extent), "sample": res["sample"]},
         "cpu_baseline": {"value": res["value"], "unit": "pair-evals/s", "cores": res["cores"], "kind": res["kind"],
                          "sample": res["sample"]},
         "e2e": {"value": res["value"], "unit": "pair-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    if not rows_mode and not args.fixed_extent and not args.no_extras and n_workload <= 20000:
+        # the CPU's exp cost depends on the data (glibc expf's underflow path), so the fixed-diameter
+        # sphere is timed beside the constant-density one (one warm-up + two gradients)
+        fx = cpu_reference_run(n_run, T, args.precision, 2, 1, fixed_extent=True, budget_s=30.0, n_workload=n_workload)
+        line["fixed_extent_40mm"] = {"value": fx["value"], "ms_per_step": fx["sec_per_gradient"] * 1e3,
+                                     "sample": fx["sample"]}
     print(json.dumps(line), flush=True)
 
 
 # ---- the B200 arm ------------------------------------------------------------------------------------------
+def nccl_log_summary(path_glob):
+    """The communicator lines of NCCL's own log (NCCL_DEBUG=INFO, NCCL_DEBUG_SUBSYS=INIT,GRAPH to a file): version,
+    ranks, whether the NVLink-SHARP (NVLS) multicast path came up, channel count."""
+    import glob
+    import re
+
+    lines = []
+    for path in sorted(glob.glob(path_glob)):
+        try:
+            with open(path, errors="replace") as f:
+                lines += f.read().splitlines()
+        except OSError:
+            pass
+    if not lines:
+        return None
+    pick = [ln.strip() for ln in lines if re.search(r"NCCL version|nranks|NVLS|Connected all|comm 0x\w+ rank|Channel \d+/\d+ :", ln)]
+    return {"nvls": any("NVLS" in ln and "disabled" not in ln.lower() for ln in lines), "log_lines": len(lines),
+            "excerpt": pick[:12]}
+
+
 def b200_arm(args):
     import numpy as np
     import torch
     import torch.distributed as dist
 
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.mode == "rows" and args.exchange == "nccl":
+        # keep NCCL's communicator log (one file per rank under gpurun_out/, summarised in the JSON line)
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH")
+        os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(ROOT, "gpurun_out", "nccl_%h_%p.log"))
+
     from paper_1907_04839_b200 import HamiltonianSystem, comm_unique_id, make_synthetic_pair
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
+    world, rank, device, oversub, backend = init_ranks()
     distributed = world > 1
-    if distributed:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     def barrier():
         if distributed:
@@ -230,6 +343,7 @@ def b200_arm(args):
         torch.cuda.synchronize()
 
     rows_mode = distributed and args.mode == "rows"
+    exchange = "p2p" if (rows_mode and oversub) else args.exchange
     n = args.n or (200000 if rows_mode else 20000)
     T = args.timesteps or (20 if rows_mode else 10)
     prec = args.precision
@@ -239,13 +353,14 @@ def b200_arm(args):
     # Template radius grows with sqrt(N/1847) so the landmark density is that of the reference's default
     # problem (synth.hpp:19-20: 1847 points on a 40 mm sphere).  At fixed 40 mm diameter N = 20 000 packs
     # 4 landmarks/mm^2 against sigma = 1.5 mm and the flow turns chaotic (|target - q0| up to 1.2 m, loss
-    # 1e16, fp32 and fp64 differ by 0.6 %): not a meaningful evaluation point.  GPU time is data-independent.
-    q0, target, _ = make_synthetic_pair(n, SIGMA, T, seed=0 if rows_mode else rank, device=local_rank,
-                                        density_scaled=True)
+    # 1e16, fp32 and fp64 differ by 0.6 %): not a meaningful evaluation point, so it is timed as an extra
+    # (`fixed_extent_40mm`, or the whole run with --fixed-extent).  GPU time is data-independent.
+    q0, target, _ = make_synthetic_pair(n, SIGMA, T, seed=0 if rows_mode else rank, device=device,
+                                        density_scaled=not args.fixed_extent)
     x0 = np.ascontiguousarray(((target - q0) / T).ravel())
 
-    system = HamiltonianSystem(SIGMA, n, 3, prec, device=local_rank, max_timesteps=T, variant=args.variant)
-    if rows_mode and args.exchange == "p2p":
+    system = HamiltonianSystem(SIGMA, n, 3, prec, device=device, max_timesteps=T, variant=args.variant)
+    if rows_mode and exchange == "p2p":
         blobs = [None] * world
         dist.all_gather_object(blobs, system.p2p_export(rank, world))
         system.p2p_connect(blobs)
@@ -254,6 +369,8 @@ def b200_arm(args):
         dist.broadcast_object_list(uid, src=0)
         system.comm_init(uid[0], rank, world)
     system.bind_registration(q0, target, LAMBDA, T)
+    if distributed:
+        dist.barrier()  # nobody's first step may store into a peer that is still binding
 
     d_x = torch.from_numpy(x0).cuda()
     d_grad = torch.empty_like(d_x)
@@ -270,6 +387,8 @@ def b200_arm(args):
         dev_ms = wall_ms = 0.0
         for _ in range(K):
             flush_l2()
+            if rows_mode:
+                dist.barrier()  # the ranks enter every step together, as one job would
             t0 = time.perf_counter()
             if device_buffers:
                 system.objective_ptrs(d_x.data_ptr(), d_grad.data_ptr(), device=True)
@@ -284,7 +403,7 @@ def b200_arm(args):
         system.objective_ptrs(h_x.data_ptr(), h_grad.data_ptr(), device=False)
     launches_per_step = system.last_eval_kernel_launches()
 
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(device)
     sampler.start()
     barrier()
     dev_ms, wall_dev = timed_pass(True)
@@ -297,10 +416,11 @@ def b200_arm(args):
     def max_over_ranks(v):
         if not distributed:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    my_dev_ms = dev_ms
     dev_ms = max_over_ranks(dev_ms)
     wall_host = max_over_ranks(wall_host)
     units_per_step = 2.0 * T * float(n) * float(n)
@@ -314,12 +434,12 @@ def b200_arm(args):
         "scaling": "strong" if rows_mode else "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
         "config": {
             "workload": (f"single registration N={n}, T={T}, row-partitioned over {world} GPUs, per-step "
-                         + ("NCCL all-gather" if args.exchange == "nccl" else "peer-push exchange (P2P stores + flags)")
+                         + ("NCCL all-gather" if exchange == "nccl" else "peer-push exchange (P2P stores + flags)")
                          if rows_mode else
                          f"single registration N={n}, T={T}, one fwd+bwd gradient per step"
                          + (f", {world} independent replicas" if distributed else "")),
             "n": n, "timesteps": T, "sigma": SIGMA, "lambda": LAMBDA, "units_per_step": "2*T*N^2",
-            "template": "Fibonacci sphere, radius 20*sqrt(N/1847) mm (constant landmark density)",
+            "template": template_label(args.fixed_extent),
             "l2": "flushed between timed steps (256 MiB write)", "variant": args.variant,
             "kernel_variant": system.lib.lms_system_kernel_names(system.handle).decode(),
         },
@@ -329,23 +449,44 @@ def b200_arm(args):
         "clocks": clocks,
         "wall_ms_per_step_device_buffers": wall_dev / K,
     }
+    if oversub:
+        line["config"]["oversubscribed"] = (f"{world} ranks share {torch.cuda.device_count()} GPU(s): a launcher / "
+                                            "exchange check, not a scaling measurement")
 
-    # ---- roofline of the dominant kernel (adjoint pair kernel), measured live with per-launch events ----
+    # ---- per-launch kernel times of every rank (events around each pair-kernel launch; separate timed pass) ----
+    system.set_kernel_timing(True)
+    fwd_ms = adj_ms = step_ms = 0.0
+    for _ in range(K):
+        flush_l2()
+        if rows_mode:
+            dist.barrier()
+        system.objective_ptrs(d_x.data_ptr(), d_grad.data_ptr(), device=True)
+        fwd_ms += system.last_kernel_ms("forward")
+        adj_ms += system.last_kernel_ms("adjoint")
+        step_ms += system.last_eval_device_ms()
+    system.set_kernel_timing(False)
+    fwd_ms /= K
+    adj_ms /= K
+    step_ms /= K
+    if rows_mode:
+        # what is left of a step after its 2T pair-kernel launches: the exchanges (all-gathers or flag waits,
+        # including the time spent waiting for the slowest rank) plus the O(N) kernels
+        mine = {"rank": rank, "ms_per_step": my_dev_ms / K, "forward_launch_ms": fwd_ms, "adjoint_launch_ms": adj_ms,
+                "pair_kernels_ms_per_step": (fwd_ms + adj_ms) * T,
+                "exchange_and_wait_ms_per_step": step_ms - (fwd_ms + adj_ms) * T}
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
+        line["per_rank"] = per_rank
+        if exchange == "nccl" and rank == 0:
+            line["nccl"] = nccl_log_summary(os.path.join(ROOT, "gpurun_out", "nccl_*.log"))
+
+    # ---- roofline of the dominant kernel (adjoint pair kernel), from the per-launch events above ----
     if rank == 0:
         peaks, peaks_src = measured_peaks()
-        system.set_kernel_timing(True)
-        fwd_ms = adj_ms = 0.0
-        for _ in range(K):
-            flush_l2()
-            system.objective_ptrs(d_x.data_ptr(), d_grad.data_ptr(), device=True)
-            fwd_ms += system.last_kernel_ms("forward")
-            adj_ms += system.last_kernel_ms("adjoint")
-        system.set_kernel_timing(False)
-        fwd_ms /= K
-        adj_ms /= K
         rows_share = 1.0 / world if rows_mode else 1.0
         pairs_per_launch = float(n) * float(n) * rows_share
         f_slots, a_slots = (FWD_SLOTS, ADJ_SLOTS) if prec == "f32" else (FWD_SLOTS_F64, ADJ_SLOTS_F64)
+        f_exec, a_exec = (FWD_EXEC, ADJ_EXEC) if prec == "f32" else (FWD_EXEC_F64, ADJ_EXEC_F64)
         lanes = 128 if prec == "f32" else 64
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         peak_slots = 148 * lanes * sm_mhz * 1e6
@@ -361,10 +502,14 @@ def b200_arm(args):
             "peak_source": f"148 SM x {lanes} lanes x sm_max_mhz {sm_mhz:.0f} MHz ({peaks_src} MEASURED_PEAKS.json)",
             "algorithmic_slots_per_pair": a_slots, "pairs_per_launch": pairs_per_launch,
             "avg_launch_ms": adj_ms,
+            # the contract counts 43 / 18 (fp64 60 / 35) slots per pair; the kernels EXECUTE fewer (hand-fused terms,
+            # branch-free exp): this is the pipe utilisation by executed lane-instructions (cf. ncu's pipe counters)
+            "executed_slots_per_pair": a_exec, "frac_executed": a_exec * pairs_per_launch / (adj_ms * 1e-3) / peak_slots,
             "traffic": (measured_traffic("adj", prec) or {}).get("bytes_per_launch") if n == 20000 and T == 10 else None,
             "traffic_source": (measured_traffic("adj", prec) or {}).get("source"),
             "forward_kernel": {"avg_launch_ms": fwd_ms, "achieved": fwd_rate / 1e12, "frac": fwd_rate / peak_slots,
-                               "algorithmic_slots_per_pair": f_slots},
+                               "algorithmic_slots_per_pair": f_slots, "executed_slots_per_pair": f_exec,
+                               "frac_executed": f_exec * pairs_per_launch / (fwd_ms * 1e-3) / peak_slots},
             "gradient": {"achieved": grad_rate / 1e12, "frac": grad_rate / peak_slots,
                          "slots_per_gradient": (f_slots + a_slots) * T * pairs_per_launch},
             "hbm": {"algorithmic_bytes_per_launch": bytes_per_launch,
@@ -383,45 +528,68 @@ def b200_arm(args):
 
     # ---- extras on rank 0 at one GPU: fp64 beside fp32, ms per L-BFGS iteration, CPU baseline ----
     if rank == 0 and not distributed and not args.no_extras:
-        if prec == "f32":
-            s64 = HamiltonianSystem(SIGMA, n, 3, "f64", device=local_rank, max_timesteps=T, variant=args.variant)
-            s64.bind_registration(q0, target, LAMBDA, T)
+        def time_steps(sys_, reps):
             for _ in range(2):
-                s64.objective_ptrs(d_x.data_ptr(), d_grad.data_ptr(), device=True)
-            ms64 = 0.0
-            reps = max(3, K // 2)
+                sys_.objective_ptrs(d_x.data_ptr(), d_grad.data_ptr(), device=True)
+            ms = 0.0
             for _ in range(reps):
                 flush_l2()
-                s64.objective_ptrs(d_x.data_ptr(), d_grad.data_ptr(), device=True)
-                ms64 += s64.last_eval_device_ms()
-            ms64 /= reps
+                sys_.objective_ptrs(d_x.data_ptr(), d_grad.data_ptr(), device=True)
+                ms += sys_.last_eval_device_ms()
+            return ms / reps
+
+        if prec == "f32":
+            s64 = HamiltonianSystem(SIGMA, n, 3, "f64", device=device, max_timesteps=T, variant=args.variant)
+            s64.bind_registration(q0, target, LAMBDA, T)
+            ms64 = time_steps(s64, max(3, K // 2))
             slots64 = (FWD_SLOTS_F64 + ADJ_SLOTS_F64) * T * float(n) * float(n)
+            exec64 = (FWD_EXEC_F64 + ADJ_EXEC_F64) * T * float(n) * float(n)
+            peak64 = 148 * 64 * float(measured_peaks()[0].get("sm_max_mhz", 1965.0)) * 1e6
             line["fp64"] = {"ms_per_step": ms64, "value": units_per_step / (ms64 * 1e-3),
-                            "frac_of_fp64_roofline": slots64 / (ms64 * 1e-3) / (148 * 64 * 1965e6)}
+                            "frac_of_fp64_roofline": slots64 / (ms64 * 1e-3) / peak64,
+                            "frac_executed": exec64 / (ms64 * 1e-3) / peak64,
+                            "note": "contract slots 35/60 per pair; executed DP-pipe ops 28/50 (branch-free exp)"}
             s64.close()
+        if not args.fixed_extent:
+            # the fixed 40 mm sphere beside the constant-density one (device time is data-independent;
+            # the CPU arm's is not)
+            fq0, ftarget, _ = make_synthetic_pair(n, SIGMA, T, seed=0, device=device, density_scaled=False)
+            sfx = HamiltonianSystem(SIGMA, n, 3, prec, device=device, max_timesteps=T, variant=args.variant)
+            sfx.bind_registration(fq0, ftarget, LAMBDA, T)
+            keep = d_x.clone()
+            d_x.copy_(torch.from_numpy(np.ascontiguousarray(((ftarget - fq0) / T).ravel())))
+            msfx = time_steps(sfx, max(3, K // 2))
+            d_x.copy_(keep)
+            sfx.close()
+            line["fixed_extent_40mm"] = {"ms_per_step": msfx, "value": units_per_step / (msfx * 1e-3)}
         # ms per L-BFGS iteration: the whole registration loop through the C ABI (lms_register: host-buffer
-        # objective + the library's host L-BFGS driver, no Python inside the loop)
+        # objective + the library's host L-BFGS driver, no Python inside the loop); every variant is run twice and
+        # both runs are reported (the first includes whatever one-time cost is left after binding)
         from paper_1907_04839_b200 import ShootingConfig, register_landmarks
 
         cfg = ShootingConfig(sigma=SIGMA, timesteps=T, lam=LAMBDA, max_iter=args.lbfgs_iters, precision=prec)
-        t0 = time.perf_counter()
-        reg = register_landmarks(q0, target, cfg, device=local_rank, system=system, already_bound=True)
-        lb_ms = (time.perf_counter() - t0) * 1e3
-        final_eval_ms = wall_host / K  # lms_register ends with one extra evaluation to leave q(1) resident
-        line["lbfgs"] = {"iterations": reg.iterations, "evaluations": reg.evaluations,
-                         "ms_per_iteration": (lb_ms - final_eval_ms) / max(reg.iterations, 1),
-                         "ms_total": lb_ms, "final_loss": reg.final_loss, "initial_loss": reg.initial_loss,
+        eval_ms = dev_ms / K
+
+        def registration(device_vectors):
+            runs = []
+            for _ in range(2):
+                t0 = time.perf_counter()
+                reg = register_landmarks(q0, target, cfg, device=device, system=system, device_vectors=device_vectors,
+                                         already_bound=True)
+                runs.append((time.perf_counter() - t0) * 1e3)
+            # lms_register[_device] ends with one extra evaluation that leaves q(1) resident
+            per_iter = [(ms - eval_ms) / max(reg.iterations, 1) for ms in runs]
+            return reg, {"iterations": reg.iterations, "evaluations": reg.evaluations,
+                         "ms_per_iteration": per_iter[1], "ms_per_iteration_first_run": per_iter[0],
+                         "ms_total": runs[1], "ms_total_first_run": runs[0],
+                         "ms_per_iteration_over_ms_per_gradient": per_iter[1] / eval_ms,
+                         "final_loss": reg.final_loss, "initial_loss": reg.initial_loss,
                          "avg_dist_before_mm": reg.avg_before, "avg_dist_after_mm": reg.avg_after}
-        # the same loop with the optimiser's vectors resident in HBM (lms_register_device)
-        t0 = time.perf_counter()
-        regd = register_landmarks(q0, target, cfg, device=local_rank, system=system, device_vectors=True,
-                                  already_bound=True)
-        lbd_ms = (time.perf_counter() - t0) * 1e3
-        line["lbfgs_device_vectors"] = {"iterations": regd.iterations, "evaluations": regd.evaluations,
-                                        "ms_per_iteration": (lbd_ms - dev_ms / K) / max(regd.iterations, 1),
-                                        "ms_total": lbd_ms, "final_loss": regd.final_loss}
+
+        _, line["lbfgs"] = registration(False)
+        _, line["lbfgs_device_vectors"] = registration(True)
         try:
-            cpu = cpu_reference_run(CPU_SAMPLE_N, T, prec, 1, 1)
+            cpu = cpu_reference_run(CPU_SAMPLE_N, T, prec, 1, 1, fixed_extent=args.fixed_extent, n_workload=n)
             line["cpu_baseline"] = {"value": cpu["value"], "unit": "pair-evals/s", "cores": cpu["cores"],
                                     "kind": cpu["kind"], "sample": cpu["sample"]}
         except Exception as e:  # the oracle is test infrastructure; its absence must not hide the GPU number
@@ -443,13 +611,7 @@ def batch_arm(args):
 
     from paper_1907_04839_b200 import BatchedRegistrations, make_template_points, rng_normals, HamiltonianSystem
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    world, rank, local_rank, oversub, backend = init_ranks()
     B, n, T = args.batch, args.n or 2000, args.timesteps or 10
     K, W = max(args.steps, 1), max(args.warmup, 3)
     q0 = np.empty((B, n, 3))
@@ -482,7 +644,7 @@ def batch_arm(args):
         wall_ms += (time.perf_counter() - t0) * 1e3
         dev_ms += br.last_eval_device_ms()
     if world > 1:
-        t = torch.tensor([dev_ms, wall_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dev_ms, wall_ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms, wall_ms = float(t[0]), float(t[1])
     units = 2.0 * T * float(n) * float(n) * B * world
@@ -508,12 +670,18 @@ def batch_arm(args):
 def main():
     args = parse_args()
     if args.impl == "reference":
-        reference_arm(args)
+        reference_arm(args)  # host cores only: rank 0 runs it, under torchrun the other ranks exit at once
+        return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if args.launch_check:
+        launch_check(args)
     elif args.batch > 0:
         batch_arm(args)
     else:
         b200_arm(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -202,7 +202,9 @@ int lms_batch_final_q(lms_system* sys, double* out);
 /* register_impl core (registration.cpp:43-93) for every problem of the batch: each problem runs its own
  * minimize (lbfgs.hpp:81-82) on a host thread; concurrent objective calls are coalesced into one batched
  * device evaluation per round.  momenta_out / warped_out: batch x n x dim; results / status: batch entries
- * (status = LMS_OK, LMS_ERR_DIVERGED or LMS_ERR_NUMERICAL per problem). */
+ * (status = LMS_OK, LMS_ERR_DIVERGED or LMS_ERR_NUMERICAL per problem).  At most LMS_BATCH_REGISTER_MAX problems
+ * per call (LMS_ERR_INVALID beyond). */
+#define LMS_BATCH_REGISTER_MAX 4096 /* problems per lms_batch_register call (one host thread each) */
 int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* momenta_out, double* warped_out,
                        lms_minimize_result* results, int* status, int* rounds_out);
 

@@ -224,7 +224,14 @@ int lms_compute_gradient(lms_system* sys, const double* q0, const double* p0, co
                          int timesteps, double* scalars, double* grad)
 {
   return guarded(sys, [&](lms::SystemBase* s) {
-    s->bind(q0, target, lambda, timesteps);
+    // the reference's entry point takes q0 / target / lambda / T on every call; binding uploads them and
+    // captures the evaluation graph, so it is skipped when they are the ones already bound
+    const size_t elems = s->cfg.n * (size_t)s->cfg.dim;
+    const bool same = s->bound && s->batch == 1 && s->lambda == lambda && s->timesteps == timesteps &&
+                      s->host_q0.size() == elems && s->host_target.size() == elems &&
+                      std::memcmp(s->host_q0.data(), q0, elems * sizeof(double)) == 0 &&
+                      std::memcmp(s->host_target.data(), target, elems * sizeof(double)) == 0;
+    if (!same) s->bind(q0, target, lambda, timesteps);
     double sc[3] = {0, 0, 0};
     s->eval(p0, grad, sc, false);
     if (scalars) std::memcpy(scalars, sc, sizeof(sc));
@@ -408,7 +415,7 @@ double batched_objective(void* user, const double* x, double* grad, size_t n)
   if (rv.submitted == rv.active)
     rv.run_round();
   else
-    rv.cv.wait(lock, [&] { return rv.round != my_round; });
+    rv.cv.wait(lock, [&] { return rv.round != my_round || rv.failure != LMS_OK; });
   if (rv.failure != LMS_OK) throw rv.failure;
   if (rv.diverged[ctx->id] >= 0) {
     ctx->diverged_step = rv.diverged[ctx->id];
@@ -427,6 +434,12 @@ int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* 
   lms::SystemBase* s = sys->impl;
   if (!s->bound) return LMS_ERR_STATE;
   const int B = s->batch;
+  // one blocking minimize per problem on its own host thread: bounded, so that a huge population cannot
+  // exhaust the process (split it into several lms_batch_register calls, or use lms_batch_eval directly)
+  if (B > LMS_BATCH_REGISTER_MAX) {
+    s->last_message = "lms_batch_register: more problems than LMS_BATCH_REGISTER_MAX host threads";
+    return LMS_ERR_INVALID;
+  }
   const size_t per = s->host_q0.size() / (size_t)B;
   Rendezvous rv;
   rv.sys = sys;
@@ -442,7 +455,7 @@ int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* 
   for (int b = 0; b < B; ++b) {
     ctx[b].rv = &rv;
     ctx[b].id = b;
-    threads.emplace_back([&, b] {
+    auto body = [&, b] {
       std::vector<double> x0(per), g(per);
       for (size_t e = 0; e < per; ++e)  // x0 = (target - q0)/T, registration.cpp:47-52
         x0[e] = (s->host_target[b * per + e] - s->host_q0[b * per + e]) / s->timesteps;
@@ -456,8 +469,16 @@ int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* 
       status[b] = rc;
       std::unique_lock<std::mutex> lock(rv.m);
       --rv.active;  // this problem no longer takes part in rounds
-      if (rv.active > 0 && rv.submitted == rv.active) rv.run_round();
-    });
+      if (rv.failure == LMS_OK && rv.active > 0 && rv.submitted == rv.active) rv.run_round();
+    };
+    try {
+      threads.emplace_back(body);
+    } catch (...) {  // std::system_error: no more threads.  Wake and fail the ones already running.
+      std::unique_lock<std::mutex> lock(rv.m);
+      rv.failure = LMS_ERR_STATE;
+      rv.cv.notify_all();
+      break;
+    }
   }
   for (auto& t : threads) t.join();
   if (rounds_out) *rounds_out = rv.rounds;

@@ -241,33 +241,50 @@ int minimize_core(Ops& ops, typename Ops::Vec x, typename Ops::Vec g, const lms_
 
       if (ls.step > 0) {
         Vec g_new = ls.wolfe ? trial_g : best_g;
+        // s and y belong to nobody until they enter the history: a throwing vector operation in between
+        // (device policy: a failed launch) must hand them back
         Vec s = ops.make(), y = ops.make();
-        ops.take_step(s, y, x, ls.step, d, g_new, g);
-        loss = ls.loss;
-        ops.copy(g, g_new);
-        const int k = result->iterations++;
-        if (hist_loss) hist_loss[k] = loss;
-        if (hist_grad_inf_norm) hist_grad_inf_norm[k] = ops.max_abs(g);
-        if (hist_step) hist_step[k] = ls.step;
-        if (hist_evals) hist_evals[k] = ls.evals;
-
-        double sy, ss, yy;
-        ops.pair_stats(s, y, &sy, &ss, &yy);  // s.y, s.s, y.y
-        const double s_norm = std::sqrt(ss);
-        const double y_norm = std::sqrt(yy);
-        if (sy > 1e-10 * s_norm * y_norm) {
-          gamma = sy / yy;
-          hist_s.push_back(s);
-          hist_y.push_back(y);
-          hist_rho.push_back(1.0 / sy);
-          if ((int)hist_s.size() > params.memory) {
-            ops.release(hist_s.front());
-            ops.release(hist_y.front());
-            hist_s.erase(hist_s.begin());
-            hist_y.erase(hist_y.begin());
-            hist_rho.erase(hist_rho.begin());
+        bool kept = false;
+        try {
+          ops.take_step(s, y, x, ls.step, d, g_new, g);
+          loss = ls.loss;
+          ops.copy(g, g_new);
+          const int k = result->iterations++;
+          if (k < params.max_iter) {  // capacity of the hist_* arrays (one record per accepted iterate)
+            if (hist_loss) hist_loss[k] = loss;
+            if (hist_grad_inf_norm) hist_grad_inf_norm[k] = ops.max_abs(g);
+            if (hist_step) hist_step[k] = ls.step;
+            if (hist_evals) hist_evals[k] = ls.evals;
           }
-        } else {
+
+          double sy, ss, yy;
+          ops.pair_stats(s, y, &sy, &ss, &yy);  // s.y, s.s, y.y
+          const double s_norm = std::sqrt(ss);
+          const double y_norm = std::sqrt(yy);
+          if (sy > 1e-10 * s_norm * y_norm) {
+            gamma = sy / yy;
+            hist_s.push_back(s);
+            kept = true;  // from here on cleanup() releases them through the history
+            hist_y.push_back(y);
+            hist_rho.push_back(1.0 / sy);
+            if ((int)hist_s.size() > params.memory) {
+              ops.release(hist_s.front());
+              ops.release(hist_y.front());
+              hist_s.erase(hist_s.begin());
+              hist_y.erase(hist_y.begin());
+              hist_rho.erase(hist_rho.begin());
+            }
+          }
+        } catch (...) {
+          if (!kept) {
+            ops.release(s);
+            ops.release(y);
+          } else if (hist_y.size() < hist_s.size()) {
+            ops.release(y);  // s made it into the history, y did not
+          }
+          throw;
+        }
+        if (!kept) {
           ops.release(s);
           ops.release(y);
         }

@@ -39,7 +39,8 @@ constexpr int kTileJ = 128;    // columns staged per shared-memory tile
 constexpr int kUnitJ = 8;      // stream-K work unit: kUnitJ columns of one row tile
 constexpr int kUnitsPerTile = kTileJ / kUnitJ;
 constexpr int kClusterSize = 16;  // CTAs per row tile in the cluster-combine kernels (non-portable cluster size)
-constexpr int kMaxPeers = 7;   // row partition: up to 8 GPUs of one NVSwitch domain
+constexpr int kMaxPeers = 7;   // row partition, peer-push transport: up to 8 GPUs of one NVSwitch domain
+constexpr int kMaxRanks = 64;  // row partition, any transport (the in-process loopback group takes up to 64)
 
 enum Mode : int { kFwd = 0, kAdj = 1, kVel = 2 };
 
@@ -78,9 +79,8 @@ struct PairArgs {
   double* mm_part;  // per-row-tile partials of sum_i |q_i(1) - target_i|^2
   unsigned long long* diverged;  // atomicMin of (step << 32 | point)
   // stream-K bookkeeping
-  T* partials;
-  int* counters;
-  int max_seg;
+  T* partials;   // 2 * gridDim.x slots of kAcc * (kThreads * R) sums (see the combine in pair_kernel)
+  int* counters; // gridDim.x arrival counters, zero between launches
   // constants, rounded on the host exactly as the reference rounds them (shooting.hpp:63-68,114-115,
   // 196,293): kexp = k_scale * log2(e) for float (ex2.approx), k_scale * log2(e) * 2^kExpBits for double (Math<double>).
   T kexp;
@@ -738,8 +738,12 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       }
       cluster.sync();  // nobody's shared memory goes away before rank 0 has read it
     } else if (cta_first != cta_last) {
-      // slot of segment `ord` of row tile rt_local: rt_local * max_seg + ord (ord = CTA index - first CTA)
-      const long long slot = rt_local * a.max_seg + ((long long)blockIdx.x - cta_first);
+      // Partial slots are indexed by the writing CTA, not by the row tile: a CTA leaves at most two partial
+      // segments per launch -- the tile its range starts in (slot 2b) and, when that is a different one, the tile
+      // it ends in (slot 2b + 1); whole tiles in between are finished alone.  2 * gridDim.x slots always suffice,
+      // whatever the row-tile count (velocity fields with many more points than landmarks, subsets of a batch).
+      const long long my_start = cells * blockIdx.x / G;
+      const long long slot = 2LL * blockIdx.x + (my_start < cell_lo ? 1 : 0);
       T* mine = a.partials + slot * (NA * BM);
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -748,10 +752,13 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       __threadfence();
       __syncthreads();
       const int nseg = (int)(cta_last - cta_first + 1);
+      // one arrival counter per shared row tile, indexed by its first CTA (unique: a CTA that covers the first
+      // cell of two row tiles covers the earlier one entirely, which is then not shared)
+      int* counter = a.counters + cta_first;
       if (tid == 0) {
-        const int prev = atomicAdd(a.counters + rt_local, 1);
+        const int prev = atomicAdd(counter, 1);
         const int last = prev == nseg - 1;
-        if (last) a.counters[rt_local] = 0;  // everyone has arrived: re-arm for the next launch
+        if (last) *counter = 0;  // everyone has arrived: re-arm for the next launch
         s_last = last;
       }
       __syncthreads();
@@ -762,11 +769,15 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         for (int r = 0; r < R; ++r)
 #pragma unroll
           for (int k = 0; k < NA; ++k) acc[r][k] = T(0);
-        // ascending segment order = ascending columns; loads of several segments are in flight together
-        const T* seg0 = a.partials + rt_local * a.max_seg * (long long)(NA * BM);
+        // ascending segment order = ascending columns; loads of several segments are in flight together.
+        // Segment 0 is the first CTA's "ends here" slot unless that CTA's range starts exactly at this tile;
+        // every later CTA starts inside this tile: its slot 2b.
+        const long long first_start = cells * cta_first / G;
+        const T* seg0 = a.partials + (2LL * cta_first) * (long long)(NA * BM);
+        const long long first_off = first_start < cell_lo ? (long long)(NA * BM) : 0;
 #pragma unroll kCombineUnroll
         for (int ord = 0; ord < nseg; ++ord) {
-          const T* theirs = seg0 + (long long)ord * (NA * BM);
+          const T* theirs = seg0 + (long long)ord * (2 * NA * BM) + (ord == 0 ? first_off : 0);
 #pragma unroll
           for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -952,6 +963,31 @@ __global__ void check_finite_planes(const T* __restrict__ src, long long stride,
   const int i = (int)(e - (long long)c * n);
   if (!isfinite(src[(long long)c * stride + i]))
     atomicMin(diverged, ((unsigned long long)(unsigned)step << 32) | 0xffffffffull);
+}
+
+// Row partition: this rank's divergence word into slot `rank` of every rank's word array ...
+struct PeerList {
+  int n;
+  long long delta[kMaxPeers];  // byte distance to each peer's mapping of the exchange arena
+};
+template <int kUnused = 0>
+__global__ void publish_diverged(const unsigned long long* __restrict__ mine, unsigned long long* slot, PeerList peers)
+{
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const unsigned long long w = *mine;
+  *slot = w;
+  for (int k = 0; k < peers.n; ++k)
+    *reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(slot) + peers.delta[k]) = w;
+}
+// ... and, after the exchange, the earliest record of all ranks back into the local word (first non-finite
+// time step wins, as in the reference's sequential loop: shooting.hpp:210-211).
+template <int kUnused = 0>
+__global__ void min_diverged(const unsigned long long* __restrict__ words, int world, unsigned long long* out)
+{
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  unsigned long long w = ~0ull;
+  for (int r = 0; r < world; ++r) w = words[r] < w ? words[r] : w;
+  *out = w;
 }
 
 // scalars[0..2] = {loss, kinetic, mismatch}: fixed ascending sum of the per-row-tile partials

@@ -153,7 +153,6 @@ LMS_DECLARE_PICKS(double, 2)
 
 struct LaunchPlan {
   int grid = 0;
-  int max_seg = 1;
   int n_row_tiles = 0;
   int n_j_tiles = 0;
   int tiles_per_problem = 1;
@@ -199,7 +198,7 @@ class System final : public SystemBase {
                       int batch_count = 1);
   template <int MODE>
   void launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchPlan& plan);
-  void ensure_partials(size_t elems, int row_tiles);
+  void alloc_partials();
   PairArgs<T> base_args() const;
 
   void upload(const double* host, T* planes, long long stride, int count, int ncomp, bool check, int step,
@@ -290,6 +289,7 @@ class System final : public SystemBase {
   char* arena_ = nullptr;
   size_t arena_bytes_ = 0;
   unsigned* p2p_flags_ = nullptr;            // [world]: slot r holds the last epoch rank r announced to this rank
+  unsigned long long* div_all_ = nullptr;    // [world]: every rank's divergence word of the running evaluation
   bool p2p_active_ = false;
   bool p2p_dirty_ = false;                   // a pair kernel ran since the last flag exchange
   unsigned p2p_epoch_ = 0;

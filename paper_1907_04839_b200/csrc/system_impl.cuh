@@ -87,6 +87,7 @@ System<T, D>::System(const lms_config& c, int batch_count)
   LMS_CUDA(cudaMallocHost(&h_scalars_, 4 * B * sizeof(double)));
   part_tiles_ = (int)(stride_ / kThreads);
   alloc_exchange_arena();
+  alloc_partials();
 }
 
 // Variant 0 picks the shapes by problem size.  From N = 16 000 on (fp32) four rows per thread pay (variant 25;
@@ -130,7 +131,7 @@ void System<T, D>::alloc_exchange_arena()
   const size_t b_adj = up(B * kState * plane * sizeof(T));
   const size_t b_grad = up(std::max(plane * D, B * (size_t)cfg.n * D) * sizeof(double));
   const size_t b_part = up(B * (size_t)part_tiles_ * sizeof(double));
-  const size_t b_flags = 256;
+  const size_t b_flags = 256 + kMaxRanks * sizeof(unsigned long long);  // arrival flags, per-rank divergence words
   arena_bytes_ = b_traj + 2 * b_adj + b_grad + 2 * b_part + b_flags;
   arena_ = dev_alloc_zero<char>(arena_bytes_);
   char* p = arena_;
@@ -141,6 +142,7 @@ void System<T, D>::alloc_exchange_arena()
   h_part_ = reinterpret_cast<double*>(p);     p += b_part;
   mm_part_ = reinterpret_cast<double*>(p);    p += b_part;
   p2p_flags_ = reinterpret_cast<unsigned*>(p);
+  div_all_ = reinterpret_cast<unsigned long long*>(p + 256);
 }
 
 template <typename T, int D>
@@ -246,12 +248,10 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
     return e ? std::max(std::atoi(e), 1) : 1;
   }();
   if (p.grid < full && p.grid > (long long)round_from * num_sms_) p.grid -= p.grid % num_sms_;
-  // partial slots are indexed (row tile, segment): a row tile is shared by at most max_seg CTAs, since every
-  // CTA owns at least floor(cells / grid) consecutive units
-  const long long per_cta_min = std::max<long long>(cells / p.grid, 1);
-  p.max_seg = (int)((units_per_row + per_cta_min - 1) / per_cta_min) + 1;
+  // partial slots are indexed by CTA (two per CTA, see the combine in pair_kernel): the buffers allocated by
+  // alloc_partials() cover the fullest grid any kernel of this handle can be launched with
   constexpr int NA = Shape<MODE, D>::kAcc;
-  p.partial_elems = (size_t)p.n_row_tiles * p.max_seg * NA * p.bm;
+  p.partial_elems = (size_t)2 * p.grid * NA * p.bm;
   // Small single problems: one cluster of kClusterSize CTAs per row tile, partial sums combined in distributed
   // shared memory (pair_kernel<..., CLUSTER>).  Every CTA sweeps n_j_tiles work units (units_per_row / 16).
   // Measured on B200, fp32, ms per gradient with / without: N = 500 0.151 / 0.172, N = 1000 0.181 / 0.197, N = 1500
@@ -267,21 +267,31 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   return p;
 }
 
+// Stream-K partial slots and arrival counters, sized ONCE for the fullest grid (SMs x resident CTAs) of the
+// kernels this handle launches: the captured evaluation graph holds these pointers, and subsets of a batch or
+// velocity fields with many more points than landmarks must never force a reallocation or outgrow them.
 template <typename T, int D>
-void System<T, D>::ensure_partials(size_t elems, int row_tiles)
+void System<T, D>::alloc_partials()
 {
-  if (elems > partials_cap_) {
-    sync();
-    dev_free(partials_);
-    partials_ = dev_alloc_zero<T>(elems);
-    partials_cap_ = elems;
-  }
-  if (row_tiles > counters_cap_) {
-    sync();
-    dev_free(counters_);
-    counters_ = dev_alloc_zero<int>(row_tiles);
-    counters_cap_ = row_tiles;
-  }
+  sync();
+  dev_free(partials_);
+  dev_free(counters_);
+  size_t elems = 0;
+  int grid_max = 0;
+  auto account = [&](const KernelChoice<T>& k, int na) {
+    int per_sm = 0;
+    LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kThreads, 0));
+    const int full = num_sms_ * std::max(per_sm, 1);
+    grid_max = std::max(grid_max, full);
+    elems = std::max(elems, (size_t)2 * full * na * kThreads * k.rows_per_thread);
+  };
+  account(k_fwd_, Shape<kFwd, D>::kAcc);
+  account(k_adj_, Shape<kAdj, D>::kAcc);
+  account(k_vel_, Shape<kVel, D>::kAcc);
+  partials_ = dev_alloc_zero<T>(elems);
+  partials_cap_ = elems;
+  counters_ = dev_alloc_zero<int>(grid_max);
+  counters_cap_ = grid_max;
 }
 
 template <typename T, int D>
@@ -325,7 +335,8 @@ void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchP
   a.n_row_tiles = plan.n_row_tiles;
   a.tiles_per_problem = plan.tiles_per_problem;
   a.n_j_tiles = plan.n_j_tiles;
-  a.max_seg = plan.max_seg;
+  if (plan.partial_elems > partials_cap_ || plan.grid > counters_cap_)
+    throw StatusError{LMS_ERR_STATE, "launch plan outgrew the stream-K partial buffers"};
   a.partials = partials_;
   a.counters = counters_;
   if (plan.cluster) {
@@ -435,7 +446,6 @@ void System<T, D>::derivatives(const double* q, const double* p, double* hq, dou
   upload(q, scratch_in_, stride_, n(), D, false, 0);
   upload(p, scratch_in_ + D * stride_, stride_, n(), D, false, 0);
   LaunchPlan plan = plan_for<kFwd>(k_fwd_, n());
-  ensure_partials(plan.partial_elems, plan.n_row_tiles);
   PairArgs<T> a = base_args();
   a.jstate = a.istate = scratch_in_;
   a.out = scratch_out_;
@@ -455,7 +465,6 @@ void System<T, D>::hamiltonian(const double* q, const double* p, double* out)
   upload(q, scratch_in_, stride_, n(), D, false, 0);
   upload(p, scratch_in_ + D * stride_, stride_, n(), D, false, 0);
   LaunchPlan plan = plan_for<kFwd>(k_fwd_, n());
-  ensure_partials(plan.partial_elems, plan.n_row_tiles);
   PairArgs<T> a = base_args();
   a.jstate = a.istate = scratch_in_;
   a.out = scratch_out_;
@@ -480,7 +489,6 @@ void System<T, D>::adjoint_step(const double* q, const double* p, const double* 
   upload(alpha, scratch_in_ + 2 * D * stride_, stride_, n(), D, false, 0);
   upload(beta, scratch_in_ + 3 * D * stride_, stride_, n(), D, false, 0);
   LaunchPlan plan = plan_for<kAdj>(k_adj_, n());
-  ensure_partials(plan.partial_elems, plan.n_row_tiles);
   PairArgs<T> a = base_args();
   a.jstate = a.istate = scratch_in_;
   a.jadj = a.iadj = scratch_in_ + kState * stride_;
@@ -525,7 +533,6 @@ void System<T, D>::integrate_forward(const double* q0, const double* p0, int tim
   upload(q0, snapshot(0), stride_, n(), D, true, 0);
   upload(p0, snapshot(0) + D * stride_, stride_, n(), D, true, 0);
   LaunchPlan plan = plan_for<kFwd>(k_fwd_, n());
-  ensure_partials(plan.partial_elems, plan.n_row_tiles);
   const T dt = T(1.0 / timesteps);  // shooting.hpp:190,196
   for (int t = 0; t < timesteps; ++t) {
     PairArgs<T> a = base_args();
@@ -587,8 +594,6 @@ void System<T, D>::bind(const double* q0, const double* target, double lambda_in
     const int te_a = row_tile_end_(kThreads * k_adj_.rows_per_thread);
     plan_fwd_ = plan_for<kFwd>(k_fwd_, n(), tb_f, std::max(te_f - tb_f, 0), batch);
     plan_adj_ = plan_for<kAdj>(k_adj_, n(), tb_a, std::max(te_a - tb_a, 0), batch);
-    ensure_partials(std::max(plan_fwd_.partial_elems, plan_adj_.partial_elems),
-                    std::max(plan_fwd_.n_row_tiles, plan_adj_.n_row_tiles));
     sync();
     if (!comm_active_) {
       // Capture the whole evaluation (2T+2 kernels) into one CUDA graph: at small N the 2T dependent
@@ -673,8 +678,25 @@ void System<T, D>::enqueue_eval(bool timed, int count, const int* d_ids)
     }
   }
   if (comm_active_) {
-    all_gather_doubles(h_part_);
-    all_gather_doubles(mm_part_);
+    // Only the rank that owns a non-finite row records the step it appeared at; the others would see it one step
+    // later through the gathered state, or not at all when it appears at the last step.  Every rank publishes its
+    // word, the words travel with the scalar partials, and every rank keeps the minimum: all ranks then report
+    // the same DivergedError(t) (shooting.hpp:210-211) and leave the optimiser together.
+    PeerList peers{};
+    if (p2p_active_) {
+      peers.n = n_peers_;
+      for (int k = 0; k < n_peers_; ++k) peers.delta[k] = peer_delta_[k];
+    }
+    publish_diverged<<<1, 32, 0, stream_>>>(d_diverged_, div_all_ + rank_, peers);
+    LMS_CUDA(cudaGetLastError());
+    ++last_eval_launches;
+    p2p_dirty_ = true;
+    gather_inplace({{reinterpret_cast<char*>(h_part_), (size_t)(part_tiles_ / world_) * sizeof(double)},
+                    {reinterpret_cast<char*>(mm_part_), (size_t)(part_tiles_ / world_) * sizeof(double)},
+                    {reinterpret_cast<char*>(div_all_), sizeof(unsigned long long)}});
+    min_diverged<<<1, 32, 0, stream_>>>(div_all_, world_, d_diverged_);
+    LMS_CUDA(cudaGetLastError());
+    ++last_eval_launches;
   }
   finalize_scalars<0><<<count, 128, 0, stream_>>>(h_part_, mm_part_, part_tiles_, lambda, d_scalars_, d_ids);
   LMS_CUDA(cudaGetLastError());
@@ -891,7 +913,6 @@ void System<T, D>::velocities(const double* q, const double* p, size_t m, const 
     return;
   }
   LaunchPlan plan = plan_for<kVel>(k_vel_, (int)m);
-  ensure_partials(plan.partial_elems, plan.n_row_tiles);
   PairArgs<T> a = base_args();
   a.jstate = scratch_in_;
   a.istate = points_[0];
@@ -916,7 +937,6 @@ void System<T, D>::warp_stored(size_t m, const double* pts, double* out)
   int cur = 0;
   if (n() > 0) {
     LaunchPlan plan = plan_for<kVel>(k_vel_, (int)m);
-    ensure_partials(plan.partial_elems, plan.n_row_tiles);
     const T dt = T(1.0 / stored_t_);  // the trajectory's own dt (flow.hpp:70)
     for (int t = 0; t < stored_t_; ++t) {
       PairArgs<T> a = base_args();
@@ -947,7 +967,10 @@ void System<T, D>::relayout_for_world(int world, int rank)
   sync();
   destroy_graph();
   bound = false;
-  if (world > 1) pick_kernels(/*partitioned=*/true);
+  if (world > 1) {
+    pick_kernels(/*partitioned=*/true);
+    alloc_partials();
+  }
   const long long new_stride = world > 1 ? partition_rows((long long)cfg.n, world, rank).stride : stride_;
   if (new_stride != stride_) {
     stride_ = new_stride;
@@ -974,7 +997,7 @@ void System<T, D>::relayout_for_world(int world, int rank)
 template <typename T, int D>
 void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
 {
-  if (world < 1 || rank < 0 || rank >= world) throw StatusError{LMS_ERR_INVALID, "bad rank/world"};
+  if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world) throw StatusError{LMS_ERR_INVALID, "bad rank/world"};
   // world == 1 normally needs no communicator; LMS_FORCE_NCCL=1 keeps the NCCL path on so that a single-GPU
   // box can exercise it (tests/test_gpu_parity.py::test_nccl_path_single_rank).
   const char* force = std::getenv("LMS_FORCE_NCCL");
@@ -992,7 +1015,8 @@ void System<T, D>::comm_init(const unsigned char* id, int rank, int world)
 template <typename T, int D>
 void System<T, D>::join_local_group(LocalGroup* group, int rank)
 {
-  if (!group || rank < 0 || rank >= group->world) throw StatusError{LMS_ERR_INVALID, "bad rank/world"};
+  if (!group || group->world > kMaxRanks || rank < 0 || rank >= group->world)
+    throw StatusError{LMS_ERR_INVALID, "bad rank/world"};
   relayout_for_world(group->world, rank);
   local_ = group;
   comm_active_ = true;

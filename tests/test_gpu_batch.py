@@ -120,3 +120,59 @@ def test_batched_two_dimensional(oracle, prec):
         loss, kin, mm, g = oracle.compute_gradient(prec, q0[b], p0[b], target[b], SIGMA, lam, T)
         assert scalars[b, 0] == pytest.approx(loss, rel=TOL[prec]) and rel_inf(grad[b], g) <= TOL[prec]
     br.close()
+
+
+@pytest.mark.parametrize("batch,n,counts", [(8, 1000, [1, 3, 5, 7]), (128, 1000, [1, 17, 100, 127]),
+                                            (128, 2000, [110, 64, 3])])
+def test_every_subset_size_fits_the_partial_buffers(batch, n, counts):
+    """Subsets re-plan the stream-K split (fewer row tiles -> more CTAs per row tile).  The partial-sum slots are
+    indexed by CTA and sized once for the fullest grid, so no subset size can outgrow them (a smaller subset used
+    to need MORE slots per row tile than the bind-time plan had reserved).  Every subset result must be bitwise the
+    result of the same problems in any other subset of the same size, and match the full evaluation to rounding;
+    a full evaluation afterwards must be bitwise the first one (nothing next to the buffers was corrupted)."""
+    from paper_1907_04839_b200 import BatchedRegistrations
+
+    T, lam = 4, 10.0
+    q0, p0, target = make_batch(batch, n, 77 + batch + n)
+    br = BatchedRegistrations(SIGMA, n, batch, 3, "f32", max_timesteps=T)
+    br.bind(q0, target, lam, T)
+    full = br.evaluate(p0)
+    finals = br.final_q()
+    rng = np.random.default_rng(5)
+    for count in counts:
+        ids = np.sort(rng.choice(batch, size=count, replace=False))
+        sub = br.evaluate(p0, ids)
+        assert (sub[2][ids] == -1).all()
+        for b in ids:
+            assert np.allclose(sub[0][b], full[0][b], rtol=2e-6)
+            assert rel_inf(sub[1][b], full[1][b]) <= 2e-6
+        again = br.evaluate(p0, ids)
+        assert np.array_equal(again[0], sub[0]) and np.array_equal(again[1], sub[1])
+    after = br.evaluate(p0)
+    assert np.array_equal(after[0], full[0]) and np.array_equal(after[1], full[1])
+    assert np.array_equal(br.final_q(), finals)
+    br.close()
+
+
+def test_batch_register_with_problems_dropping_out():
+    """lms_batch_register when the problems leave the rounds at different times (different iteration budgets are
+    not available per problem, so: very different conditioning -> different line-search lengths and one problem
+    that diverges at once): the later rounds run on shrinking subsets."""
+    from paper_1907_04839_b200 import BatchedRegistrations, LbfgsParams
+
+    batch, n, T, lam = 10, 1000, 4, 1e3
+    q0, _, target = make_batch(batch, n, 404)
+    for b in range(batch):  # problem b starts (b+1) x further from its target
+        target[b] = q0[b] + (target[b] - q0[b]) * (0.2 + 0.4 * b)
+    target[3, 11, 2] = np.inf  # x0 = (target - q0)/T is non-finite: DivergedError(0) at the first evaluation
+    br = BatchedRegistrations(SIGMA, n, batch, 3, "f32", max_timesteps=T)
+    br.bind(q0, target, lam, T)
+    res = br.register(LbfgsParams(max_iter=6, grad_tol=1e-3))
+    assert res.status[3] == 2 and (np.delete(res.status, 3) == 0).all()
+    ok = np.delete(np.arange(batch), 3)
+    assert (res.final_loss[ok] < res.initial_loss[ok]).all()
+    assert res.rounds < res.evaluations[ok].sum()
+    # the handle is still healthy: a full evaluation of the returned momenta is finite for the surviving problems
+    scalars, grad, div = br.evaluate(np.where(np.isfinite(res.momenta), res.momenta, 0.0))
+    assert np.isfinite(scalars[ok]).all() and np.isfinite(grad[ok]).all()
+    br.close()

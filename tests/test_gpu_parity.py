@@ -315,6 +315,30 @@ def test_flow_velocities_and_warp(hs, oracle, prec):
     assert rel_inf(s.warp_points(q), tq[-1]) <= tol
 
 
+def test_dense_warp_between_evaluations_keeps_the_graph_valid(hs):
+    """bind -> evaluate -> warp a point set 100x larger than the landmark set -> evaluate again: the captured
+    evaluation graph holds the stream-K partial / counter buffers, so nothing a larger launch needs may be
+    reallocated under it.  The second evaluation must be bitwise the first."""
+    n, T = 1000, 6
+    q, p, target, *_ = synth_case(n, 3, 99, spread=8.0)
+    for prec in ("f32", "f64"):
+        s = hs(n, 3, prec, max_t=T)
+        s.bind_registration(q, target, 50.0, T)
+        loss1, grad1 = s.objective(p)
+        grad1 = grad1.copy()
+        pts = np.random.default_rng(12).uniform(-9, 9, (100 * n, 3))
+        moved = s.warp_points(pts)
+        assert np.isfinite(moved).all()
+        vel = s.velocities_at_step(q, p, pts)
+        assert np.isfinite(vel).all()
+        loss2, grad2 = s.objective(p)
+        assert loss2 == loss1 and np.array_equal(grad2, grad1)
+        # and the dense warp agrees with warping in small pieces (different stream-K splits, same per-row order
+        # within a CTA range: equal to rounding)
+        piece = s.warp_points(pts[:1500])
+        assert rel_inf(moved[:1500], piece) <= TOL[prec]
+
+
 # ---- full-size checks (BASELINE.json configs[1]: N = 20 000, T = 10) ---------------------------------------
 @pytest.fixture(scope="module")
 def full_case():
@@ -387,7 +411,8 @@ def test_full_size_properties_fp64(hs, full_case):
 
 
 def test_full_size_fp32_tracks_fp64(hs, full_case):
-    """fp32 at N = 20 000 against the device's own fp64 result at the paper's initial point."""
+    """fp32 at N = 20 000 against the device's own fp64 result at the paper's initial point (the comparison with
+    the CPU oracle at this exact configuration is test_headline_config_full_gradient_vs_cpu_oracle)."""
     n, T, q0, target, p_true, x0 = full_case
     s64, s32 = hs(n, 3, "f64", max_t=T), hs(n, 3, "f32", max_t=T)
     s64.bind_registration(q0, target, 5e5, T)
@@ -396,7 +421,7 @@ def test_full_size_fp32_tracks_fp64(hs, full_case):
     l32, g32 = s32.objective(x0)
     assert l32 == pytest.approx(l64, rel=1e-5)
     assert s32.last_kinetic == pytest.approx(s64.last_kinetic, rel=1e-5)
-    assert rel_inf(g32, g64) <= 2e-5
+    assert rel_inf(g32, g64) <= 1e-5
 
 
 # ---- the optimiser end to end (BASELINE.json configs[0]) ----------------------------------------------------
@@ -643,6 +668,73 @@ def test_row_partition_loopback(hs, oracle, prec, world, n):
     group.close()
 
 
+@pytest.mark.parametrize("transport", ["loopback", "p2p"])
+def test_row_partition_ranks_agree_on_divergence(hs, transport):
+    """A state that turns non-finite in rows owned by ONE rank: every rank must raise DivergedError with the step
+    the unpartitioned evaluation reports (shooting.hpp:210-211) -- also when that is the last step, where the other
+    ranks never see the non-finite values in a gathered state.  (The ranks exchange their divergence words with
+    the scalar partials; without that they would disagree and the optimisers would part ways mid-collective.)"""
+    import threading
+
+    from paper_1907_04839_b200 import DivergedError, HamiltonianSystem, LocalGroup
+
+    n, world, prec = 1500, 2, "f32"
+    q, p, target, *_ = synth_case(n, 3, 77, spread=10.0)
+    q = q * 1e18
+    target = q.copy()
+    huge = p.copy()
+    huge[3, 0] = 1e30  # row 3 belongs to rank 0
+    plain = hs(n, 3, prec)
+    plain.bind_registration(q, target, 1.0, 6)
+    with pytest.raises(DivergedError) as want:
+        plain.objective(huge)
+    t_star = want.value.timestep
+    assert t_star >= 1
+    for T in (6, t_star):  # blow-up part-way, and at the very last step
+        plain.bind_registration(q, target, 1.0, T)
+        with pytest.raises(DivergedError) as want:
+            plain.objective(huge * (T / 6.0))  # same per-step increments
+        group = LocalGroup(world) if transport == "loopback" else None
+        ranks = [HamiltonianSystem(SIGMA, n, 3, prec, max_timesteps=6) for _ in range(world)]
+        if transport == "p2p":
+            blobs = [s.p2p_export(r, world) for r, s in enumerate(ranks)]
+            for s in ranks:
+                s.p2p_connect(blobs)
+        steps, errors = [None] * world, []
+        meet = threading.Barrier(world)
+
+        def run(r):
+            try:
+                s = ranks[r]
+                if transport == "loopback":
+                    s.join_local_group(group, r)
+                s.bind_registration(q, target, 1.0, T)
+                meet.wait(timeout=120)
+                try:
+                    s.objective(huge * (T / 6.0))
+                    steps[r] = -1
+                except DivergedError as e:
+                    steps[r] = e.timestep
+                # the handles stay usable and in step with each other
+                loss, _ = s.objective(p * 1e-3)
+                assert np.isfinite(loss)
+            except Exception as e:  # pragma: no cover
+                errors.append(e)
+                meet.abort()
+
+        threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+        assert not errors, errors
+        assert steps == [want.value.timestep] * world, (T, steps, want.value.timestep)
+        for s in ranks:
+            s.close()
+        if group is not None:
+            group.close()
+
+
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 def test_device_resident_lbfgs_matches_host_driver(prec):
     """lms_register_device (optimiser vectors in HBM) against lms_register (host vectors,
@@ -675,9 +767,34 @@ def test_device_resident_lbfgs_matches_host_driver(prec):
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-def test_full_size_full_gradient_vs_cpu_oracle(hs, oracle, full_case, prec):
-    """N = 20 000 (BASELINE configs[1]), every row: the complete objective evaluation against the CPU oracle on
-    all host threads.  T = 2 keeps the oracle's (2T+2) N^2 passes to a few seconds."""
+def test_headline_config_full_gradient_vs_cpu_oracle(hs, oracle, full_case, prec):
+    """BASELINE configs[1] itself -- N = 20 000, T = 10, lambda = 5e5, every row, at the paper's initial point
+    x0 = (target - q0)/T (registration.cpp:47-52) -- against the CPU oracle's compute_gradient
+    (shooting.hpp:277-315; (2T+2) N^2 = 8.8e9 pair evaluations, ~10 s on 16 host threads): loss, H, mismatch and
+    dL/dp0 within 1e-5 (fp32) / 1e-10 (fp64), the tolerances of BASELINE.json's north_star.  Both the call the
+    bench times (bind + objective, evaluation graph) and lms_compute_gradient are checked."""
+    n, T, q0, target, p_true, x0 = full_case
+    lam = 5e5
+    loss, kin, mm, grad = oracle.compute_gradient(prec, q0, x0, target, SIGMA, lam, T)
+    s = hs(n, 3, prec, max_t=T)
+    s.bind_registration(q0, target, lam, T)
+    got_loss, got_grad = s.objective(x0)
+    tol = TOL[prec]
+    assert got_loss == pytest.approx(loss, rel=tol)
+    assert s.last_kinetic == pytest.approx(kin, rel=tol)
+    assert s.last_mismatch == pytest.approx(mm, rel=tol)
+    assert rel_inf(got_grad.reshape(n, 3), grad) <= tol
+    r = s.compute_gradient(q0, x0, target, lam, T)
+    assert r.loss == got_loss and np.array_equal(r.grad.ravel(), got_grad)  # same graph, same bits
+    # q(1) of that evaluation against the oracle's forward flow
+    otq, _ = oracle.integrate_forward(prec, q0, x0, SIGMA, T)
+    assert rel_inf(s.final_q(), otq[-1]) <= tol
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_full_size_full_gradient_second_point(hs, oracle, full_case, prec):
+    """N = 20 000, every row, at a second evaluation point and step count (T = 2, momenta rescaled to land near
+    the target) against the CPU oracle."""
     n, _, q0, target, p_true, x0 = full_case
     T, lam = 2, 5e5
     s = hs(n, 3, prec, max_t=10)
@@ -687,6 +804,48 @@ def test_full_size_full_gradient_vs_cpu_oracle(hs, oracle, full_case, prec):
     assert r.kinetic == pytest.approx(kin, rel=TOL[prec])
     assert r.mismatch == pytest.approx(mm, rel=TOL[prec])
     assert rel_inf(r.grad, grad) <= TOL[prec]
+
+
+# ---- SPEC.md acceptance runs on the device path (long trajectories) ----------------------------------------
+def test_momentum_conservation_long_trajectory_on_device(oracle):
+    """SPEC.md acceptance 3 (:222,559): N = 100, T = 100 in fp64 -- the total momentum sum_i p_i(t) drifts by at most
+    1e-10 * sum_i |p_i(0)| over the whole trajectory; and the device trajectory equals the oracle's to 1e-10."""
+    from paper_1907_04839_b200 import HamiltonianSystem
+
+    n, T = 100, 100
+    q, p, *_ = synth_case(n, 3, 2024, spread=5.0)
+    s = HamiltonianSystem(SIGMA, n, 3, "f64", max_timesteps=T)
+    tq, tp = s.integrate_forward(q, p, T)
+    s.close()
+    drift = np.abs(tp.sum(axis=1) - p.sum(axis=0)).max()
+    assert drift <= 1e-10 * np.linalg.norm(p, axis=1).sum()
+    otq, otp = oracle.integrate_forward("f64", q, p, SIGMA, T)
+    assert rel_inf(tq, otq) <= 1e-10 and rel_inf(tp, otp) <= 1e-10
+
+
+def test_hamiltonian_drift_is_first_order_on_device(oracle):
+    """SPEC.md acceptance 2 (:223,558): explicit Euler conserves H to first order in dt -- the drift
+    |H(q(1),p(1)) - H(q0,p0)| at T = 400 is about half the drift at T = 200 (ratio in [0.4, 0.6]); both runs go
+    through the device handle (trajectory capacity 400) and match the oracle's end states."""
+    from paper_1907_04839_b200 import HamiltonianSystem
+
+    n = 200
+    q, p, *_ = synth_case(n, 3, 2025, spread=4.0)
+    s = HamiltonianSystem(SIGMA, n, 3, "f64", max_timesteps=400)
+    h0 = s.hamiltonian(q, p)
+    drifts = []
+    for T in (200, 400):
+        tq, tp = s.integrate_forward(q, p, T)
+        drifts.append(abs(s.hamiltonian(tq[-1], tp[-1]) - h0))
+        otq, otp = oracle.integrate_forward("f64", q, p, SIGMA, T)
+        assert rel_inf(tq[-1], otq[-1]) <= 1e-10 and rel_inf(tp[-1], otp[-1]) <= 1e-10
+    # a gradient through all 400 stored snapshots: the adjoint sweep at the handle's capacity
+    target = tq[-1] + 0.01
+    r = s.compute_gradient(q, p, target, 10.0, 400)
+    o = oracle.compute_gradient("f64", q, p, target, SIGMA, 10.0, 400)
+    assert r.loss == pytest.approx(o[0], rel=1e-10) and rel_inf(r.grad, o[3]) <= 1e-10
+    s.close()
+    assert drifts[0] > 0 and 0.4 <= drifts[1] / drifts[0] <= 0.6, drifts
 
 
 def test_result_document_of_a_registration_reproduces_the_warp(tmp_path):
