@@ -144,8 +144,8 @@ def test_every_subset_size_fits_the_partial_buffers(batch, n, counts):
         sub = br.evaluate(p0, ids)
         assert (sub[2][ids] == -1).all()
         for b in ids:
-            assert np.allclose(sub[0][b], full[0][b], rtol=2e-6)
-            assert rel_inf(sub[1][b], full[1][b]) <= 2e-6
+            assert np.allclose(sub[0][b], full[0][b], rtol=1e-5)
+            assert rel_inf(sub[1][b], full[1][b]) <= 1e-5  # different stream-K splits: fp32 rounding
         again = br.evaluate(p0, ids)
         assert np.array_equal(again[0], sub[0]) and np.array_equal(again[1], sub[1])
     after = br.evaluate(p0)
