@@ -51,8 +51,12 @@ typedef struct lms_config {
   int max_timesteps; /* capacity of the device-resident trajectory (T + 1 snapshots are stored) */
   int device;        /* CUDA device ordinal */
   int variant;       /* kernel variant: 0 = library default (by problem size); see lms_variant_name() */
-  int reserved;
+  int flags;         /* 0, or LMS_FLAG_* bits */
 } lms_config;
+
+/* Small single problems run the whole evaluation as one persistent cooperative kernel (csrc/small_kernels.cuh);
+ * this bit pins the tiled multi-launch path instead (A/B and tests). */
+#define LMS_FLAG_TILED_ONLY 1
 
 int lms_system_create(const lms_config* cfg, lms_system** out);
 void lms_system_destroy(lms_system* sys);

@@ -29,7 +29,7 @@ class LmsConfig(ctypes.Structure):
         ("max_timesteps", c_int),
         ("device", c_int),
         ("variant", c_int),
-        ("reserved", c_int),
+        ("flags", c_int),
     ]
 
 

@@ -10,24 +10,29 @@
 // the only global synchronisation is one grid barrier per time step.
 //
 //   rows      "slots" of RS rows (fp32: the 2 rows of a packed FFMA2 operand; fp64: 1 row) are dealt round-robin
-//             to all gridDim.x * 8 warps; a warp keeps up to RP slots (row operands + 2D running sums per row) in
-//             registers.  Row operands are warp-uniform.
+//             to gridDim.x * WR "row warps"; a row warp keeps up to RP slots (row operands + 2D running sums per
+//             row) in registers.  Row operands are warp-uniform.
 //   columns   every CTA streams the whole landmark state through shared memory in chunks of 512 (fp64: 256)
 //             columns, double buffered with bulk-async copies (cp.async.bulk + mbarrier: reads L2, so the state
-//             other CTAs wrote before the barrier is seen without any L1 concern); lane l takes columns
-//             l, l+32, ... of a chunk (consecutive lanes, consecutive words: conflict-free LDS.32).
-//   sums      per lane ascending columns, then a fixed xor-butterfly over the lanes: bitwise reproducible.
+//             other CTAs wrote before the barrier is seen without any L1 concern).  When a CTA has fewer slots
+//             than warps, WC warps share a slot: warp wc takes the 32-column groups wc, wc + WC, ... of every
+//             chunk and lane l column l of a group (consecutive lanes, consecutive words: conflict-free LDS.32).
+//   sums      per lane ascending columns, the WC column warps in ascending order through shared memory, then a
+//             fixed xor-butterfly over the lanes: bitwise reproducible.
 //   epilogue  lane r of the warp finishes the warp's row r with exactly the arithmetic of the tiled kernels'
 //             epilogues (explicit _rn operations in the reference's expression order).
-//   barrier   sense-reversing counter in global memory (the launch is cooperative: all CTAs are resident).
+//   barrier   one monotonic arrival counter in global memory (the launch is cooperative: all CTAs are resident):
+//             red.release to arrive, ld.acquire to poll; the host hands every launch the count it starts from.
 #pragma once
 
 #include "pair_kernels.cuh"
 
 namespace lms {
 
-constexpr int kSmallWarps = 8;
-constexpr int kSmallThreads = kSmallWarps * 32;
+constexpr int kSmallMaxWarps = 16;  // warps per CTA: 16 with one slot per row warp, 8 with several
+// largest n the persistent kernel is chosen for (measured crossover with the tiled path; LMS_SMALL_MAX_N overrides)
+constexpr int kSmallMaxN32 = 4000;
+constexpr int kSmallMaxN64 = 3000;
 
 template <typename T>
 struct SmallShape {
@@ -46,10 +51,12 @@ struct SmallArgs {
   T* hp0;                 // H_p(q0, p0): D planes
   const T* target;        // D planes
   double* grad_out;       // row-major double n x D
-  double* warp_part;      // 2 x (gridDim.x * kSmallWarps): per-warp partials of sum p.hp and of the mismatch
+  double* warp_part;      // 2 x (gridDim.x * wr): per-row-warp partials of sum p.hp and of the mismatch
   double* scalars;        // {loss, kinetic, mismatch}
   unsigned long long* diverged;
-  unsigned* barrier;      // [0] arrival count, [32] generation (separate 128-byte lines), zero at first use
+  unsigned* barrier;      // monotonic arrival counter
+  unsigned bar_base;      // its value when this launch starts (the host counts gridDim.x * barriers per launch)
+  int wr, wc;             // row warps per CTA x column warps per slot (wr * wc <= warps per CTA)
   int n;
   int n_chunks;
   int timesteps;
@@ -58,24 +65,19 @@ struct SmallArgs {
 };
 
 // All CTAs of the (cooperative) launch meet here.  Everything written before it -- by the generic proxy -- is
-// visible after it to generic loads that bypass L1 (__ldcg) and to bulk-async copies (async proxy).
-__device__ __forceinline__ void small_grid_barrier(unsigned* bar)
+// visible after it to generic loads that bypass L1 (__ldcg) and to bulk-async copies (async proxy).  `target` is
+// the counter value that means "everybody has arrived" (advanced by gridDim.x per barrier; wrap-safe compare).
+__device__ __forceinline__ void small_grid_barrier(unsigned* bar, unsigned& target)
 {
+  target += gridDim.x;
   asm volatile("fence.proxy.async.global;" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 32;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      atomicExch(bar, 0u);  // nobody touches the count again before the generation moves
-      __threadfence();
-      atomicAdd(bar + 32, 1u);
-    } else {
-      while (*gen == g) {
-      }
-    }
-    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+    } while ((int)(seen - target) < 0);
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
   __syncthreads();
@@ -86,8 +88,8 @@ __device__ __forceinline__ void small_grid_barrier(unsigned* bar)
 template <typename T, int D, int MODE, int RP>
 __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __restrict__ state,
                                            const T* __restrict__ adj_in, T* __restrict__ out, unsigned epi, int step_no,
-                                           T* tile, unsigned long long* bars, unsigned& buf, unsigned& wait_parity,
-                                           double& hsum, double& msum, const double* exp_tbl)
+                                           T* tile, T* part, unsigned long long* bars, unsigned& buf,
+                                           unsigned& wait_parity, double& hsum, double& msum, const double* exp_tbl)
 {
   using S = Shape<MODE, D>;
   constexpr int NC = S::kColComps, NR = S::kRowComps, NA = S::kAcc;
@@ -96,13 +98,17 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
   constexpr int CH = SmallShape<T>::kChunk;
   constexpr int NCMAX = 4 * D;
   const int lane = threadIdx.x & 31;
-  const int GW = gridDim.x * kSmallWarps;
-  const int gw = blockIdx.x * kSmallWarps + (threadIdx.x >> 5);
+  const int warp = threadIdx.x >> 5;
+  const int wc = warp / a.wr;            // column part of this warp (>= a.wc: a spare warp, no work)
+  const int GW = gridDim.x * a.wr;       // row warps of the launch
+  const int gw = blockIdx.x * a.wr + (warp - wc * a.wr);
   const int slots = (a.n + RS - 1) / RS;
-  int my = 0;  // slots this warp owns: gw, gw + GW, ...
+  int my = 0;  // slots this warp works on: gw, gw + GW, ...
+  if (wc < a.wc) {
 #pragma unroll
-  for (int i = 0; i < RP; ++i)
-    if (gw + i * GW < slots) my = i + 1;
+    for (int i = 0; i < RP; ++i)
+      if (gw + i * GW < slots) my = i + 1;
+  }
 
   auto plane = [&](int k) -> const T* {
     if constexpr (MODE == kAdj)
@@ -160,8 +166,9 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
     mbar_wait(&bars[buf], (wait_parity >> buf) & 1u);
     wait_parity ^= 1u << buf;
     const T* tb = tile + (long long)buf * NCMAX * CH;
+    const int jstep = 32 * a.wc;
 #pragma unroll 2
-    for (int jj = lane; jj < CH; jj += 32) {
+    for (int jj = wc * 32 + lane; jj < CH; jj += jstep) {
       T cj[NC];
 #pragma unroll
       for (int k = 0; k < NC; ++k) cj[k] = tb[k * CH + jj];
@@ -192,6 +199,27 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
         acc[i][0][k] = (T)(flip ? -acc2[i][k].x : acc2[i][k].x);
         acc[i][RS - 1][k] = (T)(flip ? -acc2[i][k].y : acc2[i][k].y);
       }
+  }
+  if (a.wc > 1) {
+    // the column warps of a slot meet in shared memory: ascending column part, lane by lane (RP == 1 here)
+    if (wc > 0 && my > 0) {
+      T* mine = part + ((long long)(wc - 1) * a.wr + (warp - wc * a.wr)) * (RS * NA * 32);
+#pragma unroll
+      for (int h = 0; h < RS; ++h)
+#pragma unroll
+        for (int k = 0; k < NA; ++k) mine[(h * NA + k) * 32 + lane] = acc[0][h][k];
+    }
+    __syncthreads();
+    if (wc == 0 && my > 0) {
+      for (int c = 1; c < a.wc; ++c) {
+        const T* theirs = part + ((long long)(c - 1) * a.wr + warp) * (RS * NA * 32);
+#pragma unroll
+        for (int h = 0; h < RS; ++h)
+#pragma unroll
+          for (int k = 0; k < NA; ++k) acc[0][h][k] += theirs[(h * NA + k) * 32 + lane];
+      }
+    }
+    if (wc > 0) my = 0;  // only the first column warp of a slot finishes its rows
   }
 #pragma unroll
   for (int i = 0; i < RP; ++i) {
@@ -266,11 +294,14 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
   }
 }
 
-template <typename T, int D, int RP>
-__global__ void __launch_bounds__(kSmallThreads, 1) small_eval_kernel(const SmallArgs<T> a)
+template <typename T, int D, int RP, int W>
+__global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T> a)
 {
+  constexpr int kThreadsHere = 32 * W;
+  constexpr int RS = SmallShape<T>::kRowsPerSlot;
   extern __shared__ __align__(128) unsigned char small_smem[];
   T* tile = reinterpret_cast<T*>(small_smem);
+  __shared__ __align__(16) T part[(W - 1) * RS * Shape<kFwd, D>::kAcc * 32];  // column-warp partial sums
   __shared__ __align__(8) unsigned long long bars[2];
   __shared__ double exp_tbl[kExpEntries];
   if (threadIdx.x == 0) {
@@ -285,8 +316,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_eval_kernel(const Smal
   {
     T* p_planes = a.traj + (long long)D * a.stride;
     const long long total = (long long)a.n * D;
-    for (long long e = (long long)blockIdx.x * kSmallThreads + threadIdx.x; e < total;
-         e += (long long)gridDim.x * kSmallThreads) {
+    for (long long e = (long long)blockIdx.x * kThreadsHere + threadIdx.x; e < total;
+         e += (long long)gridDim.x * kThreadsHere) {
       const int i = (int)(e / D);
       const int c = (int)(e - (long long)i * D);
       const T v = (T)a.x[e];
@@ -294,33 +325,34 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_eval_kernel(const Smal
       if (!Math<T>::finite(v)) atomicMin(a.diverged, 0xffffffffull);  // step 0
     }
   }
-  small_grid_barrier(a.barrier);
+  unsigned bar_target = a.bar_base;
+  small_grid_barrier(a.barrier, bar_target);
 
   unsigned buf = 0, wait_parity = 0;
   double hsum = 0.0, msum = 0.0;
   const int Tn = a.timesteps;
   const int lane = threadIdx.x & 31;
-  const int GW = gridDim.x * kSmallWarps;
-  const int gw = blockIdx.x * kSmallWarps + (threadIdx.x >> 5);
+  const int warp = threadIdx.x >> 5;
+  const int GW = gridDim.x * a.wr;
   // forward Euler flow, T+1 snapshots kept for the adjoint (shooting.hpp:199-212)
   for (int t = 0; t < Tn; ++t) {
     const unsigned epi = kEpiEuler | (t == 0 ? kEpiFirstStep : 0u) | (t == Tn - 1 ? kEpiLastStep : 0u);
     small_step<T, D, kFwd, RP>(a, a.traj + (long long)t * a.snap_elems, nullptr,
-                               a.traj + (long long)(t + 1) * a.snap_elems, epi, t + 1, tile, bars, buf, wait_parity, hsum,
-                               msum, exp_tbl);
+                               a.traj + (long long)(t + 1) * a.snap_elems, epi, t + 1, tile, part, bars, buf,
+                               wait_parity, hsum, msum, exp_tbl);
     if (t == Tn - 1) {
-      // per-warp partials of the two double sums: lanes hold their rows' terms; fixed butterfly
+      // per-row-warp partials of the two double sums: lanes hold their rows' terms; fixed butterfly
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) {
         hsum += __shfl_xor_sync(0xffffffffu, hsum, off);
         msum += __shfl_xor_sync(0xffffffffu, msum, off);
       }
-      if (lane == 0) {
-        a.warp_part[gw] = hsum;
-        a.warp_part[GW + gw] = msum;
+      if (lane == 0 && warp < a.wr) {
+        a.warp_part[blockIdx.x * a.wr + warp] = hsum;
+        a.warp_part[GW + blockIdx.x * a.wr + warp] = msum;
       }
     }
-    small_grid_barrier(a.barrier);
+    small_grid_barrier(a.barrier, bar_target);
   }
   // loss = H + lambda*mismatch, H = 1/2 sum_i p_i . hp_i  (shooting.hpp:286-288): warp 0 of CTA 0 adds the per-warp
   // partials (lane-strided ascending, then the fixed butterfly)
@@ -347,12 +379,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_eval_kernel(const Smal
   T* adj_out = a.adj1;
   for (int t = Tn - 1; t >= 0; --t) {
     small_step<T, D, kAdj, RP>(a, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
-                               kEpiEuler | (t == 0 ? kEpiGradOut : 0u), t, tile, bars, buf, wait_parity, hsum, msum,
+                               kEpiEuler | (t == 0 ? kEpiGradOut : 0u), t, tile, part, bars, buf, wait_parity, hsum, msum,
                                exp_tbl);
     T* tmp = adj_in;
     adj_in = adj_out;
     adj_out = tmp;
-    if (t > 0) small_grid_barrier(a.barrier);
+    if (t > 0) small_grid_barrier(a.barrier, bar_target);
   }
 }
 

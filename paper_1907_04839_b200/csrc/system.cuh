@@ -19,6 +19,7 @@
 #include "../../include/lmshoot_b200.h"
 #include "nccl_dyn.h"
 #include "pair_kernels.cuh"
+#include "small_kernels.cuh"
 
 namespace lms {
 
@@ -217,6 +218,8 @@ class System final : public SystemBase {
   void relayout_for_world(int world, int rank);
   void pick_kernels(bool partitioned);
   void alloc_exchange_arena();
+  void plan_small();
+  void launch_small();
   void p2p_exchange();
   void p2p_disconnect();
 
@@ -278,6 +281,17 @@ class System final : public SystemBase {
   int graph_launches_ = 0;
   std::vector<cudaEvent_t> events_;
   cudaEvent_t ev_begin_ = nullptr, ev_end_ = nullptr;
+
+  // small single problems: the whole evaluation as one persistent cooperative kernel (small_kernels.cuh)
+  bool small_enabled_ = true;     // LMS_SMALL=0 pins the tiled path
+  int small_max_n_ = 0;           // largest n the persistent kernel is chosen for (LMS_SMALL_MAX_N)
+  bool use_small_ = false;        // decided at bind
+  int small_grid_ = 0, small_threads_ = 0, small_wr_ = 0, small_wc_ = 1;
+  unsigned small_bar_count_ = 0;  // arrivals the barrier counter has seen so far (host-side mirror)
+  size_t small_smem_ = 0;
+  void (*small_fn_)(SmallArgs<T>) = nullptr;
+  double* warp_part_ = nullptr;   // 2 x (SMs x kSmallMaxWarps) per-row-warp scalar partials
+  unsigned* small_bar_ = nullptr; // grid barrier: monotonic arrival counter
 
   // row partition (multi-GPU)
   int rank_ = 0, world_ = 1;

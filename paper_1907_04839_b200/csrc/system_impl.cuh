@@ -47,6 +47,10 @@ System<T, D>::System(const lms_config& c, int batch_count)
   num_sms_ = prop.multiProcessorCount;
   if (const char* e = std::getenv("LMS_PDL")) pdl_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("LMS_CLUSTER")) cluster_combine_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LMS_SMALL")) small_enabled_ = std::atoi(e) != 0;
+  if (c.flags & LMS_FLAG_TILED_ONLY) small_enabled_ = false;
+  small_max_n_ = sizeof(T) == 4 ? kSmallMaxN32 : kSmallMaxN64;
+  if (const char* e = std::getenv("LMS_SMALL_MAX_N")) small_max_n_ = std::atoi(e);
   LMS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   LMS_CUDA(cudaEventCreate(&ev_begin_));
   LMS_CUDA(cudaEventCreate(&ev_end_));
@@ -86,6 +90,8 @@ System<T, D>::System(const lms_config& c, int batch_count)
   d_ids_ = dev_alloc_zero<int>(B);
   LMS_CUDA(cudaMallocHost(&h_scalars_, 4 * B * sizeof(double)));
   part_tiles_ = (int)(stride_ / kThreads);
+  warp_part_ = dev_alloc_zero<double>((size_t)2 * num_sms_ * kSmallMaxWarps);
+  small_bar_ = dev_alloc_zero<unsigned>(64);
   alloc_exchange_arena();
   alloc_partials();
 }
@@ -163,6 +169,8 @@ System<T, D>::~System()
   dev_free(points_[1]);
   dev_free(partials_);
   dev_free(counters_);
+  dev_free(warp_part_);
+  dev_free(small_bar_);
   dev_free(d_scalars_);
   dev_free(d_io_);
   dev_free(d_x_);
@@ -371,6 +379,87 @@ void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchP
     LMS_CUDA(cudaGetLastError());
   }
   ++last_eval_launches;
+}
+
+// ---- small problems: one persistent cooperative kernel per evaluation (small_kernels.cuh) -----------------------
+template <typename T, int D>
+void System<T, D>::plan_small()
+{
+  use_small_ = false;
+  if (!small_enabled_ || batch != 1 || comm_active_ || n() <= 0 || n() > small_max_n_) return;
+  constexpr int RS = SmallShape<T>::kRowsPerSlot;
+  constexpr int CH = SmallShape<T>::kChunk;
+  if (stride_ % CH != 0) return;
+  const int slots = ceil_div(n(), RS);
+  const int grid = std::min(num_sms_, slots);
+  const int per_cta = ceil_div(slots, grid);  // slots of the busiest CTA
+  if (per_cta <= kSmallMaxWarps) {
+    // one slot per row warp; the spare warps split the columns of a slot (wc warps each)
+    small_fn_ = small_eval_kernel<T, D, 1, 16>;
+    small_threads_ = 32 * 16;
+    small_wr_ = per_cta;
+    small_wc_ = kSmallMaxWarps / per_cta;
+  } else {
+    // several slots per warp, eight warps (the register budget of 16 does not hold two slots)
+    const int rp = ceil_div(per_cta, 8);
+    switch (rp) {
+      case 2: small_fn_ = small_eval_kernel<T, D, 2, 8>; break;
+      case 3: small_fn_ = small_eval_kernel<T, D, 3, 8>; break;
+      case 4: small_fn_ = small_eval_kernel<T, D, 4, 8>; break;
+      default: return;  // more rows per warp than the register budget holds: the tiled path
+    }
+    small_threads_ = 32 * 8;
+    small_wr_ = 8;
+    small_wc_ = 1;
+  }
+  int coop = 0;
+  LMS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cfg.device));
+  if (!coop) return;
+  small_smem_ = (size_t)2 * (4 * D) * CH * sizeof(T);
+  LMS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(small_fn_), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)small_smem_));
+  int per_sm = 0;
+  LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fn_, small_threads_, small_smem_));
+  if (per_sm < 1) return;
+  small_grid_ = grid;
+  use_small_ = true;
+}
+
+template <typename T, int D>
+void System<T, D>::launch_small()
+{
+  LMS_CUDA(cudaMemsetAsync(d_diverged_, 0xff, sizeof(unsigned long long), stream_));
+  SmallArgs<T> a{};
+  a.x = d_x_;
+  a.traj = traj_;
+  a.stride = stride_;
+  a.snap_elems = (long long)kState * stride_;
+  a.adj0 = adj_[0];
+  a.adj1 = adj_[1];
+  a.hp0 = hp0_;
+  a.target = target_;
+  a.grad_out = d_grad_;
+  a.warp_part = warp_part_;
+  a.scalars = d_scalars_;
+  a.diverged = d_diverged_;
+  a.barrier = small_bar_;
+  a.bar_base = small_bar_count_;
+  small_bar_count_ += (unsigned)small_grid_ * (unsigned)(2 * timesteps);  // 1 + T + (T-1) barriers per launch
+  a.wr = small_wr_;
+  a.wc = small_wc_;
+  a.n = n();
+  a.n_chunks = ceil_div(n(), SmallShape<T>::kChunk);
+  a.timesteps = timesteps;
+  a.kexp = kexp_;
+  a.inv_sig2 = inv_sig2_;
+  a.dt = dt_;
+  a.two_lambda = two_lambda_;
+  a.lambda = lambda;
+  void* args[] = {&a};
+  LMS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(small_fn_), dim3(small_grid_), dim3(small_threads_),
+                                       args, small_smem_, stream_));
+  last_eval_launches = 1;
+  final_adj_ = timesteps & 1;
 }
 
 // ---- host <-> planes ---------------------------------------------------------------------------------------
@@ -585,6 +674,7 @@ void System<T, D>::bind(const double* q0, const double* target, double lambda_in
     }
   traj0_is_q0_ = false;
   stored_t_ = -1;
+  use_small_ = false;
   if (n() > 0) {
     upload(q0, q0_, stride_, n(), D, false, 0, batch, bs_vec_);
     upload(target, target_, stride_, n(), D, false, 0, batch, bs_vec_);
@@ -595,6 +685,7 @@ void System<T, D>::bind(const double* q0, const double* target, double lambda_in
     plan_fwd_ = plan_for<kFwd>(k_fwd_, n(), tb_f, std::max(te_f - tb_f, 0), batch);
     plan_adj_ = plan_for<kAdj>(k_adj_, n(), tb_a, std::max(te_a - tb_a, 0), batch);
     sync();
+    plan_small();
     if (!comm_active_) {
       // Capture the whole evaluation (2T+2 kernels) into one CUDA graph: at small N the 2T dependent
       // launches are pure latency (SURVEY.md §7 "Small-N latency").
@@ -821,7 +912,9 @@ void System<T, D>::eval(const double* x, double* grad, double* scalars, bool dev
                            stream_));
   LMS_CUDA(cudaEventRecord(ev_begin_, stream_));
   const bool timed = kernel_timing;
-  if (graph_ && !timed) {
+  if (use_small_ && !timed) {
+    launch_small();
+  } else if (graph_ && !timed) {
     LMS_CUDA(cudaGraphLaunch(graph_, stream_));
     last_eval_launches = graph_launches_;
   } else {

@@ -70,7 +70,7 @@ class HamiltonianSystem:
     scratch; nothing O(N^2) is ever allocated (K is never materialised).
     """
 
-    def __init__(self, sigma, n, dim=3, precision="f64", device=0, max_timesteps=40, variant=0):
+    def __init__(self, sigma, n, dim=3, precision="f64", device=0, max_timesteps=40, variant=0, tiled_only=False):
         if dim not in (2, 3):
             raise ShapeError("dimension must be 2 or 3")  # shooting.hpp:358
         if not sigma > 0:
@@ -80,7 +80,9 @@ class HamiltonianSystem:
         self.lib = _lib.load()
         self.sigma, self.n, self.dim, self.precision = float(sigma), int(n), int(dim), precision
         self.device, self.max_timesteps, self.variant = int(device), int(max_timesteps), int(variant)
-        cfg = _lib.LmsConfig(PRECISION[precision], dim, n, sigma, max_timesteps, device, variant, 0)
+        # tiled_only: LMS_FLAG_TILED_ONLY, pins the multi-launch tiled path (small problems otherwise run the whole
+        # evaluation as one persistent kernel)
+        cfg = _lib.LmsConfig(PRECISION[precision], dim, n, sigma, max_timesteps, device, variant, 1 if tiled_only else 0)
         handle = c_void_p()
         _lib.check(self.lib.lms_system_create(ctypes.byref(cfg), ctypes.byref(handle)))
         self.handle = handle

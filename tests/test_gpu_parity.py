@@ -23,10 +23,11 @@ def hs():
 
     cache = {}
 
-    def make(n, dim, prec, max_t=40, variant=0):
-        key = (n, dim, prec, max_t, variant)
+    def make(n, dim, prec, max_t=40, variant=0, tiled_only=False):
+        key = (n, dim, prec, max_t, variant, tiled_only)
         if key not in cache:
-            cache[key] = HamiltonianSystem(SIGMA, n, dim, prec, device=0, max_timesteps=max_t, variant=variant)
+            cache[key] = HamiltonianSystem(SIGMA, n, dim, prec, device=0, max_timesteps=max_t, variant=variant,
+                                           tiled_only=tiled_only)
         return cache[key]
 
     yield make
@@ -40,8 +41,12 @@ def test_extension_is_loaded_and_runs_on_device(hs):
     from paper_1907_04839_b200 import _lib
 
     assert isinstance(_lib.load(), ctypes.CDLL)
-    s = hs(64, 3, "f32")
     q, p, target, *_ = synth_case(64, 3, 1)
+    s = hs(64, 3, "f32")  # small problems: the whole evaluation is one persistent kernel
+    s.compute_gradient(q, p, target, 10.0, 4)
+    assert s.last_eval_kernel_launches() == 1
+    assert s.last_eval_device_ms() > 0.0
+    s = hs(64, 3, "f32", tiled_only=True)  # the tiled path: conversion + T forward + scalars + T adjoint launches
     s.compute_gradient(q, p, target, 10.0, 4)
     assert s.last_eval_kernel_launches() == 2 * 4 + 2
     assert s.last_eval_device_ms() > 0.0
@@ -95,10 +100,13 @@ def test_per_function_parity_vs_oracle(hs, oracle, prec, n):
 @pytest.mark.parametrize("prec", ["f32", "f64"])
 @pytest.mark.parametrize("n,T,lam", [(1, 1, 3.0), (2, 5, 10.0), (7, 10, 10.0), (257, 10, 10.0), (1000, 10, 10.0),
                                      (1000, 10, 5e5), (600, 40, 5e5)])
-def test_compute_gradient_parity(hs, oracle, prec, n, T, lam):
+@pytest.mark.parametrize("tiled_only", [False, True], ids=["persistent", "tiled"])
+def test_compute_gradient_parity(hs, oracle, prec, n, T, lam, tiled_only):
+    """The complete objective evaluation against the oracle, through both device paths: the persistent
+    one-launch kernel small problems select by default, and the tiled stream-K kernels (pinned)."""
     tol = TOL[prec]
     q, p, target, *_ = synth_case(n, 3, 200 + n + T, spread=8.0)
-    s = hs(n, 3, prec)
+    s = hs(n, 3, prec, tiled_only=tiled_only)
     r = s.compute_gradient(q, p, target, lam, T)
     loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, SIGMA, lam, T)
     assert r.loss == pytest.approx(loss, rel=tol)
@@ -106,6 +114,35 @@ def test_compute_gradient_parity(hs, oracle, prec, n, T, lam):
     assert r.mismatch == pytest.approx(mm, rel=tol)
     assert rel_inf(r.grad, grad) <= tol
     assert rel_inf(s.final_q(), oracle.integrate_forward(prec, q, p, SIGMA, T)[0][-1]) <= tol
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 255, 256, 257, 511, 512, 513, 1184, 1185, 2369, 2900])
+def test_persistent_kernel_edge_sizes(hs, oracle, prec, dim, n):
+    """The persistent path at the sizes where its decomposition changes: fewer rows than one warp's slot, one
+    chunk of staged columns +- 1 (512 fp32 / 256 fp64), one and two slots per warp (148 SMs x 8 warps = 1184 warps),
+    an odd last row of a packed pair; odd T and even T end in different adjoint buffers.  Checked against the
+    oracle, against the tiled path (same epilogue arithmetic, different summation order) and for run-to-run bits."""
+    tol = TOL[prec]
+    # constant landmark density (a denser cloud than ~500 per 14^dim box makes the flow itself ill-conditioned in fp32)
+    q, p, target, *_ = synth_case(n, dim, 4000 + n + dim, spread=7.0 * max(1.0, (n / 500.0) ** (1.0 / dim)))
+    s = hs(n, dim, prec, max_t=8)
+    tiled = hs(n, dim, prec, max_t=8, tiled_only=True)
+    for T in (3, 4):
+        r = s.compute_gradient(q, p, target, 25.0, T)
+        assert s.last_eval_kernel_launches() == 1
+        loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, SIGMA, 25.0, T)
+        assert r.loss == pytest.approx(loss, rel=tol) and r.kinetic == pytest.approx(kin, rel=tol, abs=1e-300)
+        assert r.mismatch == pytest.approx(mm, rel=tol)
+        assert rel_inf(r.grad, grad) <= tol
+        assert rel_inf(s.final_q(), oracle.integrate_forward(prec, q, p, SIGMA, T)[0][-1]) <= tol
+        again = s.compute_gradient(q, p, target, 25.0, T)
+        assert again.loss == r.loss and np.array_equal(again.grad, r.grad)
+        rt = tiled.compute_gradient(q, p, target, 25.0, T)
+        assert rt.loss == pytest.approx(r.loss, rel=tol) and rel_inf(rt.grad, r.grad) <= tol
+    # the stored trajectory of the persistent evaluation feeds the warp exactly like the tiled one's
+    assert rel_inf(s.warp_points(q), s.final_q()) <= 3 * tol  # two different fp32 summation orders
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
@@ -219,10 +256,11 @@ def test_gradient_vs_finite_differences_on_device(hs):
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-def test_bitwise_run_to_run_determinism(hs, prec):
+@pytest.mark.parametrize("tiled_only", [False, True], ids=["persistent", "tiled"])
+def test_bitwise_run_to_run_determinism(hs, prec, tiled_only):
     n = 3000
     q, p, target, *_ = synth_case(n, 3, 5, spread=10.0)
-    s = hs(n, 3, prec)
+    s = hs(n, 3, prec, tiled_only=tiled_only)
     s.bind_registration(q, target, 5e5, 10)
     first = s.objective(p)
     for _ in range(3):
@@ -231,7 +269,7 @@ def test_bitwise_run_to_run_determinism(hs, prec):
     # a fresh handle (new buffers, new graph) gives the same bits too
     from paper_1907_04839_b200 import HamiltonianSystem
 
-    other = HamiltonianSystem(SIGMA, n, 3, prec, max_timesteps=10)
+    other = HamiltonianSystem(SIGMA, n, 3, prec, max_timesteps=10, tiled_only=tiled_only)
     other.bind_registration(q, target, 5e5, 10)
     fresh = other.objective(p)
     other.close()
@@ -522,7 +560,7 @@ def test_nccl_path_single_rank(hs, monkeypatch, prec):
 
     n, T = 1500, 6
     q, p, target, *_ = synth_case(n, 3, 77, spread=9.0)
-    plain = hs(n, 3, prec)
+    plain = hs(n, 3, prec, tiled_only=True)  # the partitioned ranks run the tiled kernels: compare like with like
     plain.bind_registration(q, target, 100.0, T)
     want = plain.objective(p)
     monkeypatch.setenv("LMS_FORCE_NCCL", "1")
@@ -627,7 +665,7 @@ def test_row_partition_loopback(hs, oracle, prec, world, n):
 
     T, lam = 5, 100.0
     q, p, target, *_ = synth_case(n, 3, 500 + n + world, spread=10.0 if n < 10000 else 60.0)
-    plain = hs(n, 3, prec)
+    plain = hs(n, 3, prec, tiled_only=True)  # the partitioned ranks run the tiled kernels: compare like with like
     plain.bind_registration(q, target, lam, T)
     want_loss, want_grad = plain.objective(p)
     want_q = plain.final_q()
@@ -684,7 +722,7 @@ def test_row_partition_ranks_agree_on_divergence(hs, transport):
     target = q.copy()
     huge = p.copy()
     huge[3, 0] = 1e30  # row 3 belongs to rank 0
-    plain = hs(n, 3, prec)
+    plain = hs(n, 3, prec, tiled_only=True)  # the partitioned ranks run the tiled kernels: compare like with like
     plain.bind_registration(q, target, 1.0, 6)
     with pytest.raises(DivergedError) as want:
         plain.objective(huge)
@@ -884,7 +922,7 @@ def test_row_partition_peer_push_in_process(hs, oracle, prec, world, n):
 
     T, lam = 5, 100.0
     q, p, target, *_ = synth_case(n, 3, 900 + n + world, spread=10.0 if n < 10000 else 60.0)
-    plain = hs(n, 3, prec)
+    plain = hs(n, 3, prec, tiled_only=True)  # the partitioned ranks run the tiled kernels: compare like with like
     plain.bind_registration(q, target, lam, T)
     want_loss, want_grad = plain.objective(p)
     want_q = plain.final_q()
@@ -996,7 +1034,7 @@ def test_row_partition_peer_push_across_processes(hs, prec):
     q = rng.uniform(-10, 10, (n, 3))
     p = 0.75 * rng.normal(size=(n, 3))
     target = q + 0.5 * rng.normal(size=(n, 3))
-    plain = hs(n, 3, prec)
+    plain = hs(n, 3, prec, tiled_only=True)  # the partitioned ranks run the tiled kernels: compare like with like
     plain.bind_registration(q, target, lam, T)
     want_loss, want_grad = plain.objective(p)
     tol = 1e-12 if prec == "f64" else 2e-6
