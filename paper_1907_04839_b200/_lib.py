@@ -12,7 +12,8 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_longlong, c_size_t, c_u
 from .errors import CommError, CudaError, DivergedError, NumericalError, ShapeError, StateError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblmshoot_b200.so")
+# LMS_LIB_PATH: a side-by-side measurement build of the same library (see __graft_entry__.py, LMS_BUILD_TAG)
+LIB_PATH = os.environ.get("LMS_LIB_PATH") or os.path.join(_HERE, "liblmshoot_b200.so")
 
 LMS_OK, LMS_ERR_SHAPE, LMS_ERR_DIVERGED, LMS_ERR_INVALID = 0, 1, 2, 3
 LMS_ERR_NUMERICAL, LMS_ERR_CUDA, LMS_ERR_STATE, LMS_ERR_COMM = 4, 5, 6, 7

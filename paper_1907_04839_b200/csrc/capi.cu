@@ -498,6 +498,17 @@ int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* 
   return LMS_OK;
 }
 
+#ifdef LMS_SMALL_TRACE
+// measurement builds only (scripts/small_trace.py): the phase timestamps the persistent kernel left in the scratch
+int lms_debug_read_trace(lms_system* sys, unsigned long long* out, size_t count)
+{
+  return guarded(sys, [&](lms::SystemBase* s) {
+    if (cudaMemcpy(out, s->staging_scratch(), count * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+      throw lms::StatusError{LMS_ERR_CUDA, "trace read failed"};
+  });
+}
+#endif
+
 // ---- synthetic inputs ----
 namespace {
 // rng.hpp:14-48: mt19937_64 with the explicit uniform / Box-Muller transforms (pairs, spare kept).

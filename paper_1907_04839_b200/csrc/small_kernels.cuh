@@ -12,9 +12,11 @@
 //   rows      "slots" of RS rows (fp32: the 2 rows of a packed FFMA2 operand; fp64: 1 row) are dealt round-robin
 //             to gridDim.x * WR "row warps"; a row warp keeps up to RP slots (row operands + 2D running sums per
 //             row) in registers.  Row operands are warp-uniform.
-//   columns   every CTA streams the whole landmark state through shared memory in chunks of 512 (fp64: 256)
-//             columns, double buffered with bulk-async copies (cp.async.bulk + mbarrier: reads L2, so the state
-//             other CTAs wrote before the barrier is seen without any L1 concern).  When a CTA has fewer slots
+//   columns   every CTA pulls the whole landmark state into shared memory in chunks of 512 (fp64: 256) columns with
+//             bulk-async copies (cp.async.bulk + one mbarrier per chunk: reads L2, so the state other CTAs wrote
+//             before the barrier is seen without any L1 concern).  All chunks of a step are in flight at once (up
+//             to 8: N <= 4096 fp32 / 2048 fp64) and a warp waits only for the chunk it is about to read, so there
+//             is no CTA-wide synchronisation inside a sweep.  When a CTA has fewer slots
 //             than warps, WC warps share a slot: warp wc takes the 32-column groups wc, wc + WC, ... of every
 //             chunk and lane l column l of a group (consecutive lanes, consecutive words: conflict-free LDS.32).
 //   sums      per lane ascending columns, the WC column warps in ascending order through shared memory, then a
@@ -30,13 +32,33 @@
 namespace lms {
 
 constexpr int kSmallMaxWarps = 16;  // warps per CTA: 16 with one slot per row warp, 8 with several
-// largest n the persistent kernel is chosen for (measured crossover with the tiled path; LMS_SMALL_MAX_N overrides)
-constexpr int kSmallMaxN32 = 4000;
-constexpr int kSmallMaxN64 = 3000;
+// Largest n the persistent kernel is chosen for (LMS_SMALL_MAX_N overrides): the measured crossover with the tiled
+// path in fp32 (ms per gradient, T = 10, persistent / tiled: N = 1000 0.107 / 0.217, 2000 0.195 / 0.265, 3000 0.364 /
+// 0.414, 4000 0.564 / 0.550), and the shared-memory capacity for the staged state in fp64 (N = 2000 0.427 / 0.443).
+constexpr int kSmallMaxN32 = 3500;
+constexpr int kSmallMaxN64 = 2048;
+
+// LMS_SMALL_TRACE: phase timestamps (globaltimer, ns) of CTA 0 into SmallArgs::trace -- a measurement build only
+// (scripts/small_trace.py); the shipped library compiles the macro to nothing.
+#ifdef LMS_SMALL_TRACE
+#define LMS_TRACE_POINT(a, idx)                                                  \
+  do {                                                                           \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (a).trace != nullptr) {           \
+      unsigned long long t_;                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                      \
+      (a).trace[(idx)] = t_;                                                     \
+    }                                                                            \
+  } while (0)
+#else
+#define LMS_TRACE_POINT(a, idx) \
+  do {                          \
+  } while (0)
+#endif
 
 template <typename T>
 struct SmallShape {
   static constexpr int kChunk = sizeof(T) == 4 ? 512 : 256;  // columns per staged chunk
+  static constexpr int kMaxChunks = 8;                        // chunk buffers (all resident during a step)
   static constexpr int kRowsPerSlot = sizeof(T) == 4 ? 2 : 1;
 };
 
@@ -57,12 +79,25 @@ struct SmallArgs {
   unsigned* barrier;      // monotonic arrival counter
   unsigned bar_base;      // its value when this launch starts (the host counts gridDim.x * barriers per launch)
   int wr, wc;             // row warps per CTA x column warps per slot (wr * wc <= warps per CTA)
+  unsigned long long* trace;  // LMS_SMALL_TRACE builds: 8 timestamps per step; else null
   int n;
   int n_chunks;
   int timesteps;
   T kexp, inv_sig2, dt, two_lambda;
   double lambda;
 };
+
+// Bulk copy global -> the same shared-memory offset of every CTA in cta_mask, completing on the mbarrier at the
+// same offset in each of them.
+__device__ __forceinline__ void bulk_g2s_multicast(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                                   unsigned short cta_mask)
+{
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
+      : "memory");
+}
 
 // All CTAs of the (cooperative) launch meet here.  Everything written before it -- by the generic proxy -- is
 // visible after it to generic loads that bypass L1 (__ldcg) and to bulk-async copies (async proxy).  `target` is
@@ -78,9 +113,9 @@ __device__ __forceinline__ void small_grid_barrier(unsigned* bar, unsigned& targ
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
     } while ((int)(seen - target) < 0);
-    asm volatile("fence.proxy.async.global;" ::: "memory");
   }
   __syncthreads();
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // before this thread's bulk-async reads of that data
 }
 
 // One time step for the rows this warp owns.  MODE kFwd: state -> out = next snapshot (Euler, shooting.hpp:205-211)
@@ -88,9 +123,10 @@ __device__ __forceinline__ void small_grid_barrier(unsigned* bar, unsigned& targ
 template <typename T, int D, int MODE, int RP>
 __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __restrict__ state,
                                            const T* __restrict__ adj_in, T* __restrict__ out, unsigned epi, int step_no,
-                                           T* tile, T* part, unsigned long long* bars, unsigned& buf,
-                                           unsigned& wait_parity, double& hsum, double& msum, const double* exp_tbl)
+                                           T* tile, T* part, unsigned long long* bars, unsigned& phase,
+                                           double& hsum, double& msum, const double* exp_tbl, int trace_base)
 {
+  LMS_TRACE_POINT(a, trace_base + 0);
   using S = Shape<MODE, D>;
   constexpr int NC = S::kColComps, NR = S::kRowComps, NA = S::kAcc;
   constexpr bool F32 = sizeof(T) == 4;
@@ -116,13 +152,31 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
     else
       return state + (long long)k * a.stride;
   };
-  auto issue = [&](int c, unsigned b) {  // thread 0 only
-    mbar_expect_tx(&bars[b], (unsigned)(NC * CH * sizeof(T)));
-#pragma unroll
-    for (int k = 0; k < NC; ++k)
-      bulk_g2s(tile + ((long long)b * NCMAX + k) * CH, plane(k) + (long long)c * CH, (unsigned)(CH * sizeof(T)), &bars[b]);
-  };
-  if (threadIdx.x == 0) issue(0, buf);  // buffer `buf` was last read before the previous __syncthreads
+  // Every chunk of this step's state goes into its own buffer, all in flight together: one bulk copy per
+  // (chunk, component plane), issued by lanes 0..NC-1 of warp 0 side by side; lane 0's arrive.expect_tx is a
+  // chunk barrier's one arrival, so its phase cannot complete before every byte has been expected and delivered.
+  // (All warps passed the grid barrier's __syncthreads since they last read these buffers.)
+  // All 148 CTAs pull the same bytes at the same moment, and the L2 -> SM fabric (not latency) is what the first
+  // chunk then waits for (measured: 96 KB per CTA take 3 us at N = 2000).  Launched as thread-block clusters, the
+  // CTAs of a cluster share the fetch: piece (chunk, plane) is requested by ONE of them and multicast into the
+  // same buffer offset of all (and completes on the same mbarrier offset of all), so L2 serves 1/cluster-size of
+  // the traffic.
+  unsigned cl_rank, cl_size;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(cl_rank));
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(cl_size));
+  if (warp == 0) {
+    for (int c = 0; c < a.n_chunks; ++c) {
+      if (lane == 0) mbar_expect_tx(&bars[c], (unsigned)(NC * CH * sizeof(T)));
+      if (lane < NC) {
+        T* dst = tile + ((long long)c * NCMAX + lane) * CH;
+        const T* src = plane(lane) + (long long)c * CH;
+        if (cl_size == 1)
+          bulk_g2s(dst, src, (unsigned)(CH * sizeof(T)), &bars[c]);
+        else if ((unsigned)(c * NC + lane) % cl_size == cl_rank)
+          bulk_g2s_multicast(dst, src, (unsigned)(CH * sizeof(T)), &bars[c], (unsigned short)((1u << cl_size) - 1u));
+      }
+    }
+  }
 
   // ---- row operands (warp-uniform; read past L1: other CTAs wrote them before the grid barrier) ----
   T rv[RP][RS][NR];
@@ -160,34 +214,67 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
       for (int k = 0; k < NA; ++k) acc[i][0][k] = T(0);
   }
 
-  // ---- sweep the columns, chunk by chunk ----
-  for (int c = 0; c < a.n_chunks; ++c) {
-    if (c + 1 < a.n_chunks && threadIdx.x == 0) issue(c + 1, buf ^ 1u);
-    mbar_wait(&bars[buf], (wait_parity >> buf) & 1u);
-    wait_parity ^= 1u << buf;
-    const T* tb = tile + (long long)buf * NCMAX * CH;
-    const int jstep = 32 * a.wc;
-#pragma unroll 2
-    for (int jj = wc * 32 + lane; jj < CH; jj += jstep) {
-      T cj[NC];
-#pragma unroll
-      for (int k = 0; k < NC; ++k) cj[k] = tb[k * CH + jj];
+  // ---- sweep the columns: this warp's 32-column groups wc, wc + WC, ... of the whole staged state ----
+  // U groups are loaded and evaluated together -- U independent dependency chains (LDS -> r^2 -> ex2 -> sums) in
+  // one basic block, which is what lets the few warps of a CTA keep the FMA pipe busy.  A chunk is waited for the
+  // first time one of its groups comes up.
+  constexpr int GPC = CH / 32;  // groups per chunk
+  constexpr int U = F32 ? (MODE == kAdj ? 2 : 4) : (MODE == kAdj ? 1 : 2);
+  if (my > 0) {
+    const int G = a.n_chunks * GPC;
+    int waited = 0;  // chunks [0, waited) have landed
+    auto need = [&](int g_last) {
+      const int c = g_last / GPC;
+      while (waited <= c) {
+        mbar_wait(&bars[waited], phase);
+        ++waited;
+      }
+    };
+    auto col_ptr = [&](int g) -> const T* {
+      const int c = g / GPC;
+      return tile + (long long)c * NCMAX * CH + (g - c * GPC) * 32 + lane;
+    };
+    auto evaluate = [&](const T(&cj)[NC]) {
       if constexpr (F32) {
         float2 cj2[NC];
 #pragma unroll
         for (int k = 0; k < NC; ++k) cj2[k] = splat2((float)cj[k]);
 #pragma unroll
         for (int i = 0; i < RP; ++i)
-          if (i < my) pair_term_packed<D, MODE>(ri2[i], cj2, acc2[i], kexp2, ns2, neg1);
+          if (RP == 1 || i < my) pair_term_packed<D, MODE>(ri2[i], cj2, acc2[i], kexp2, ns2, neg1);
       } else {
 #pragma unroll
         for (int i = 0; i < RP; ++i)
-          if (i < my) pair_term<T, D, MODE>(rv[i][0], cj, acc[i][0], a.kexp, a.inv_sig2, exp_tbl);
+          if (RP == 1 || i < my) pair_term<T, D, MODE>(rv[i][0], cj, acc[i][0], a.kexp, a.inv_sig2, exp_tbl);
       }
+    };
+    int g = wc;
+#ifdef LMS_SMALL_TRACE
+    if (g < G) need(g);
+    LMS_TRACE_POINT(a, trace_base + 1);
+#endif
+    for (; g + (U - 1) * a.wc < G; g += U * a.wc) {
+      need(g + (U - 1) * a.wc);
+      T cj[U][NC];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const T* cp = col_ptr(g + u * a.wc);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) cj[u][k] = cp[k * CH];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) evaluate(cj[u]);
     }
-    __syncthreads();
-    buf ^= 1u;
+    for (; g < G; g += a.wc) {
+      need(g);
+      T cj[NC];
+      const T* cp = col_ptr(g);
+#pragma unroll
+      for (int k = 0; k < NC; ++k) cj[k] = cp[k * CH];
+      evaluate(cj);
+    }
   }
+  phase ^= 1u;  // every chunk barrier completed one phase
 
   // ---- row sums: fixed butterfly over the lanes ----
   if constexpr (F32) {
@@ -200,23 +287,29 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
         acc[i][RS - 1][k] = (T)(flip ? -acc2[i][k].y : acc2[i][k].y);
       }
   }
+  LMS_TRACE_POINT(a, trace_base + 2);
   if (a.wc > 1) {
-    // the column warps of a slot meet in shared memory: ascending column part, lane by lane (RP == 1 here)
+    // the column warps of a slot meet in shared memory: ascending column part, lane by lane
+    constexpr int PER = RP * RS * NA * 32;  // one warp's partial sums
     if (wc > 0 && my > 0) {
-      T* mine = part + ((long long)(wc - 1) * a.wr + (warp - wc * a.wr)) * (RS * NA * 32);
+      T* mine = part + ((long long)(wc - 1) * a.wr + (warp - wc * a.wr)) * PER;
 #pragma unroll
-      for (int h = 0; h < RS; ++h)
+      for (int i = 0; i < RP; ++i)
 #pragma unroll
-        for (int k = 0; k < NA; ++k) mine[(h * NA + k) * 32 + lane] = acc[0][h][k];
+        for (int h = 0; h < RS; ++h)
+#pragma unroll
+          for (int k = 0; k < NA; ++k) mine[((i * RS + h) * NA + k) * 32 + lane] = acc[i][h][k];
     }
     __syncthreads();
     if (wc == 0 && my > 0) {
       for (int c = 1; c < a.wc; ++c) {
-        const T* theirs = part + ((long long)(c - 1) * a.wr + warp) * (RS * NA * 32);
+        const T* theirs = part + ((long long)(c - 1) * a.wr + warp) * PER;
 #pragma unroll
-        for (int h = 0; h < RS; ++h)
+        for (int i = 0; i < RP; ++i)
 #pragma unroll
-          for (int k = 0; k < NA; ++k) acc[0][h][k] += theirs[(h * NA + k) * 32 + lane];
+          for (int h = 0; h < RS; ++h)
+#pragma unroll
+            for (int k = 0; k < NA; ++k) acc[i][h][k] += theirs[((i * RS + h) * NA + k) * 32 + lane];
       }
     }
     if (wc > 0) my = 0;  // only the first column warp of a slot finishes its rows
@@ -236,6 +329,7 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
     }
   }
 
+  LMS_TRACE_POINT(a, trace_base + 3);
   // ---- epilogue: lane i*RS+h finishes row (i, h) ----
 #pragma unroll
   for (int i = 0; i < RP; ++i) {
@@ -301,19 +395,22 @@ __global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T
   constexpr int RS = SmallShape<T>::kRowsPerSlot;
   extern __shared__ __align__(128) unsigned char small_smem[];
   T* tile = reinterpret_cast<T*>(small_smem);
-  __shared__ __align__(16) T part[(W - 1) * RS * Shape<kFwd, D>::kAcc * 32];  // column-warp partial sums
-  __shared__ __align__(8) unsigned long long bars[2];
+  __shared__ __align__(16) T part[(W - 1) * RP * RS * Shape<kFwd, D>::kAcc * 32];  // column-warp partial sums
+  __shared__ __align__(8) unsigned long long bars[SmallShape<T>::kMaxChunks];
   __shared__ double exp_tbl[kExpEntries];
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int c = 0; c < SmallShape<T>::kMaxChunks; ++c) mbar_init(&bars[c], 1);
     mbar_fence_init();
   }
   if constexpr (sizeof(T) == 8) {
     if (threadIdx.x < kExpEntries) exp_tbl[threadIdx.x] = kExp2Table64[threadIdx.x * (64 / kExpEntries)];
   }
-  // p0[i][c] = T(x[i*D+c])  (registration.cpp:61-63); non-finite p0 -> DivergedError(0) (shooting.hpp:185-186)
+  // p0[i][c] = T(x[i*D+c])  (registration.cpp:61-63); non-finite p0 -> DivergedError(0) (shooting.hpp:185-186).
+  // The divergence word is re-armed here (CTA 0, before the first barrier) and non-finite inputs are recorded
+  // after it, so no separate memset launch precedes the kernel.
+  bool bad_input = false;
   {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.diverged = ~0ull;
     T* p_planes = a.traj + (long long)D * a.stride;
     const long long total = (long long)a.n * D;
     for (long long e = (long long)blockIdx.x * kThreadsHere + threadIdx.x; e < total;
@@ -322,13 +419,14 @@ __global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T
       const int c = (int)(e - (long long)i * D);
       const T v = (T)a.x[e];
       p_planes[(long long)c * a.stride + i] = v;
-      if (!Math<T>::finite(v)) atomicMin(a.diverged, 0xffffffffull);  // step 0
+      bad_input = bad_input || !Math<T>::finite(v);
     }
   }
   unsigned bar_target = a.bar_base;
   small_grid_barrier(a.barrier, bar_target);
+  if (bad_input) atomicMin(a.diverged, 0xffffffffull);  // step 0
 
-  unsigned buf = 0, wait_parity = 0;
+  unsigned phase = 0;  // parity the chunk barriers complete next
   double hsum = 0.0, msum = 0.0;
   const int Tn = a.timesteps;
   const int lane = threadIdx.x & 31;
@@ -338,8 +436,9 @@ __global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T
   for (int t = 0; t < Tn; ++t) {
     const unsigned epi = kEpiEuler | (t == 0 ? kEpiFirstStep : 0u) | (t == Tn - 1 ? kEpiLastStep : 0u);
     small_step<T, D, kFwd, RP>(a, a.traj + (long long)t * a.snap_elems, nullptr,
-                               a.traj + (long long)(t + 1) * a.snap_elems, epi, t + 1, tile, part, bars, buf,
-                               wait_parity, hsum, msum, exp_tbl);
+                               a.traj + (long long)(t + 1) * a.snap_elems, epi, t + 1, tile, part, bars, phase, hsum,
+                               msum, exp_tbl, 8 * t);
+    LMS_TRACE_POINT(a, 8 * t + 4);
     if (t == Tn - 1) {
       // per-row-warp partials of the two double sums: lanes hold their rows' terms; fixed butterfly
 #pragma unroll
@@ -353,6 +452,7 @@ __global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T
       }
     }
     small_grid_barrier(a.barrier, bar_target);
+    LMS_TRACE_POINT(a, 8 * t + 5);
   }
   // loss = H + lambda*mismatch, H = 1/2 sum_i p_i . hp_i  (shooting.hpp:286-288): warp 0 of CTA 0 adds the per-warp
   // partials (lane-strided ascending, then the fixed butterfly)
@@ -379,13 +479,17 @@ __global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T
   T* adj_out = a.adj1;
   for (int t = Tn - 1; t >= 0; --t) {
     small_step<T, D, kAdj, RP>(a, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
-                               kEpiEuler | (t == 0 ? kEpiGradOut : 0u), t, tile, part, bars, buf, wait_parity, hsum, msum,
-                               exp_tbl);
+                               kEpiEuler | (t == 0 ? kEpiGradOut : 0u), t, tile, part, bars, phase, hsum, msum, exp_tbl,
+                               8 * (2 * Tn - 1 - t));
+    LMS_TRACE_POINT(a, 8 * (2 * Tn - 1 - t) + 4);
     T* tmp = adj_in;
     adj_in = adj_out;
     adj_out = tmp;
     if (t > 0) small_grid_barrier(a.barrier, bar_target);
+    LMS_TRACE_POINT(a, 8 * (2 * Tn - 1 - t) + 5);
   }
+  // nobody leaves while a multicast of a cluster peer may still be landing in its shared memory
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 }  // namespace lms

@@ -96,6 +96,7 @@ class SystemBase {
                           const int* ids) = 0;
   virtual void final_q_batch(double* out) = 0;
   virtual cudaStream_t stream_handle() const = 0;
+  virtual const double* staging_scratch() const = 0;  // device scratch of the host<->plane conversions (trace builds read it)
   int batch = 1;
   // scratch owned by the device-resident L-BFGS driver (device_lbfgs.cu), kept across lms_register_device calls:
   // cudaMalloc / cudaFree cost milliseconds (and synchronise the device) next to an 8 ms evaluation
@@ -187,6 +188,7 @@ class System final : public SystemBase {
                   const int* ids) override;
   void final_q_batch(double* out) override;
   cudaStream_t stream_handle() const override { return stream_; }
+  const double* staging_scratch() const override { return d_io_; }
 
  private:
   static constexpr int kState = 2 * D;  // planes per (q,p) or (alpha,beta) state
@@ -287,6 +289,7 @@ class System final : public SystemBase {
   int small_max_n_ = 0;           // largest n the persistent kernel is chosen for (LMS_SMALL_MAX_N)
   bool use_small_ = false;        // decided at bind
   int small_grid_ = 0, small_threads_ = 0, small_wr_ = 0, small_wc_ = 1;
+  int small_cluster_ = 1, small_grid_cap_ = 0;  // thread-block cluster size sharing the state fetch (TMA multicast)
   unsigned small_bar_count_ = 0;  // arrivals the barrier counter has seen so far (host-side mirror)
   size_t small_smem_ = 0;
   void (*small_fn_)(SmallArgs<T>) = nullptr;

@@ -389,46 +389,86 @@ void System<T, D>::plan_small()
   if (!small_enabled_ || batch != 1 || comm_active_ || n() <= 0 || n() > small_max_n_) return;
   constexpr int RS = SmallShape<T>::kRowsPerSlot;
   constexpr int CH = SmallShape<T>::kChunk;
-  if (stride_ % CH != 0) return;
+  if (stride_ % CH != 0 || ceil_div(n(), CH) > SmallShape<T>::kMaxChunks) return;  // every chunk gets its own buffer
   const int slots = ceil_div(n(), RS);
   const int grid = std::min(num_sms_, slots);
   const int per_cta = ceil_div(slots, grid);  // slots of the busiest CTA
-  if (per_cta <= kSmallMaxWarps) {
-    // one slot per row warp; the spare warps split the columns of a slot (wc warps each)
-    small_fn_ = small_eval_kernel<T, D, 1, 16>;
-    small_threads_ = 32 * 16;
-    small_wr_ = per_cta;
-    small_wc_ = kSmallMaxWarps / per_cta;
-  } else {
-    // several slots per warp, eight warps (the register budget of 16 does not hold two slots)
-    const int rp = ceil_div(per_cta, 8);
-    switch (rp) {
-      case 2: small_fn_ = small_eval_kernel<T, D, 2, 8>; break;
-      case 3: small_fn_ = small_eval_kernel<T, D, 3, 8>; break;
-      case 4: small_fn_ = small_eval_kernel<T, D, 4, 8>; break;
-      default: return;  // more rows per warp than the register budget holds: the tiled path
-    }
-    small_threads_ = 32 * 8;
-    small_wr_ = 8;
-    small_wc_ = 1;
-  }
+  // One slot per row warp, sixteen warps; the spare warps split the columns of a slot (wc warps each).  (Several
+  // slots per warp on eight warps -- fewer shared-memory loads per pair, half the warps -- measured slower at every
+  // size the staged state fits: N = 2000 fp32 0.226 vs 0.206 ms, N = 3000 0.476 vs 0.380 ms.)
+  if (per_cta > kSmallMaxWarps) return;
+  const int rp = 1;
+  small_fn_ = small_eval_kernel<T, D, 1, 16>;
+  small_threads_ = 32 * 16;
+  small_wr_ = per_cta;
+  small_wc_ = kSmallMaxWarps / per_cta;
   int coop = 0;
   LMS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cfg.device));
   if (!coop) return;
-  small_smem_ = (size_t)2 * (4 * D) * CH * sizeof(T);
+  small_smem_ = (size_t)ceil_div(n(), CH) * (4 * D) * CH * sizeof(T);
   LMS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(small_fn_), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)small_smem_));
   int per_sm = 0;
   LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fn_, small_threads_, small_smem_));
   if (per_sm < 1) return;
-  small_grid_ = grid;
+  // Thread-block clusters share the state fetch (TMA multicast, small_kernels.cuh): the largest cluster size that
+  // still keeps (nearly) every SM busy.  Cluster launches must be whole clusters, so the grid is rounded up to one
+  // (CTAs without rows still fetch their share and take part in the barriers).
+  static const int force_cs = [] {
+    const char* e = std::getenv("LMS_SMALL_CLUSTER");  // experiment knob: cluster size (1 = no clusters)
+    return e ? std::atoi(e) : 0;
+  }();
+  small_cluster_ = 1;
+  for (int cs : {8, 4, 2}) {
+    if (force_cs > 0 && cs != force_cs) continue;
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(num_sms_ / cs * cs);
+    lc.blockDim = dim3(small_threads_);
+    lc.dynamicSmemBytes = small_smem_;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, reinterpret_cast<const void*>(small_fn_), &lc) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    const int cap = clusters * cs;
+    if (cap >= std::min(grid, num_sms_ * 7 / 8) || force_cs > 0) {
+      small_cluster_ = cs;
+      small_grid_cap_ = cap;
+      break;
+    }
+  }
+  if (small_cluster_ > 1) {
+    // re-plan the rows for the cluster-aligned grid
+    const int g = std::min(small_grid_cap_, (int)round_up(grid, small_cluster_));
+    const int pc = ceil_div(slots, g);
+    if (rp == 1 && pc <= kSmallMaxWarps) {
+      small_wr_ = pc;
+      small_wc_ = kSmallMaxWarps / pc;
+      small_grid_ = g;
+    } else if (rp > 1 && ceil_div(pc, rp) <= 8) {
+      small_wr_ = ceil_div(pc, rp);
+      small_wc_ = 8 / small_wr_;
+      small_grid_ = g;
+    } else {
+      small_cluster_ = 1;  // the smaller grid would need another kernel shape: stay unclustered
+      small_grid_ = grid;
+    }
+  } else {
+    small_grid_ = grid;
+  }
   use_small_ = true;
 }
 
 template <typename T, int D>
 void System<T, D>::launch_small()
 {
-  LMS_CUDA(cudaMemsetAsync(d_diverged_, 0xff, sizeof(unsigned long long), stream_));
   SmallArgs<T> a{};
   a.x = d_x_;
   a.traj = traj_;
@@ -447,6 +487,11 @@ void System<T, D>::launch_small()
   small_bar_count_ += (unsigned)small_grid_ * (unsigned)(2 * timesteps);  // 1 + T + (T-1) barriers per launch
   a.wr = small_wr_;
   a.wc = small_wc_;
+#ifdef LMS_SMALL_TRACE
+  a.trace = reinterpret_cast<unsigned long long*>(d_io_);  // staging scratch: idle during an evaluation
+#else
+  a.trace = nullptr;
+#endif
   a.n = n();
   a.n_chunks = ceil_div(n(), SmallShape<T>::kChunk);
   a.timesteps = timesteps;
@@ -455,9 +500,21 @@ void System<T, D>::launch_small()
   a.dt = dt_;
   a.two_lambda = two_lambda_;
   a.lambda = lambda;
-  void* args[] = {&a};
-  LMS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(small_fn_), dim3(small_grid_), dim3(small_threads_),
-                                       args, small_smem_, stream_));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(small_grid_);
+  lc.blockDim = dim3(small_threads_);
+  lc.dynamicSmemBytes = small_smem_;
+  lc.stream = stream_;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the kernel's grid barrier relies on it
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = small_cluster_;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = small_cluster_ > 1 ? 2 : 1;
+  LMS_CUDA(cudaLaunchKernelEx(&lc, small_fn_, a));
   last_eval_launches = 1;
   final_adj_ = timesteps & 1;
 }

@@ -131,7 +131,8 @@ def test_persistent_kernel_edge_sizes(hs, oracle, prec, dim, n):
     tiled = hs(n, dim, prec, max_t=8, tiled_only=True)
     for T in (3, 4):
         r = s.compute_gradient(q, p, target, 25.0, T)
-        assert s.last_eval_kernel_launches() == 1
+        # the persistent kernel holds the whole state in shared memory: up to 4096 landmarks in fp32, 2048 in fp64
+        assert s.last_eval_kernel_launches() == (1 if n <= (4096 if prec == "f32" else 2048) else 2 * T + 2)
         loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, SIGMA, 25.0, T)
         assert r.loss == pytest.approx(loss, rel=tol) and r.kinetic == pytest.approx(kin, rel=tol, abs=1e-300)
         assert r.mismatch == pytest.approx(mm, rel=tol)
