@@ -196,7 +196,12 @@ int lms_mismatch_sq(lms_system* sys, const double* a, const double* b, double* o
 
 int lms_bind_registration(lms_system* sys, const double* q0, const double* target, double lambda, int timesteps)
 {
-  return guarded(sys, [&](lms::SystemBase* s) { s->bind(q0, target, lambda, timesteps); });
+  return guarded(sys, [&](lms::SystemBase* s) {
+    s->bind(q0, target, lambda, timesteps);
+    // the device-resident optimiser's workspace (lms_register_device): allocated and warmed once per handle here,
+    // not inside the first registration
+    lms::prepare_device_lbfgs(s, 10 /* LbfgsParams::memory default, lbfgs.hpp:12 */);
+  });
 }
 
 int lms_objective_eval(lms_system* sys, const double* x, double* grad, double* loss, double* kinetic,
@@ -334,12 +339,20 @@ int lms_p2p_connect(lms_system* sys, const unsigned char* blobs)
 }
 
 // ---- register_impl core (registration.cpp:43-93) over the bound objective and lms_minimize ----
-static double bound_objective(void* user, const double* x, double* grad, size_t)
+namespace {
+struct BoundCall {
+  lms_system* sys;
+  std::vector<double> last_x;  // the point of the last evaluation: its trajectory is the one resident in HBM
+};
+}  // namespace
+
+static double bound_objective(void* user, const double* x, double* grad, size_t n)
 {
-  lms_system* sys = static_cast<lms_system*>(user);
+  BoundCall* call = static_cast<BoundCall*>(user);
   double loss = 0;
-  int rc = lms_objective_eval(sys, x, grad, &loss, nullptr, nullptr);
+  int rc = lms_objective_eval(call->sys, x, grad, &loss, nullptr, nullptr);
   if (rc != LMS_OK) throw rc;  // unwinds through lms_minimize like DivergedError does through minimize
+  call->last_x.assign(x, x + n);
   return loss;
 }
 
@@ -353,17 +366,22 @@ int lms_register(lms_system* sys, const lms_lbfgs_params* params, double* moment
   std::vector<double> x0(nd), g(nd);
   for (size_t e = 0; e < nd; ++e) x0[e] = (s->host_target[e] - s->host_q0[e]) / s->timesteps;  // registration.cpp:47-52
   int rc;
+  BoundCall call{sys, {}};
   try {
-    rc = lms_minimize(bound_objective, sys, nd, x0.data(), params, momenta_out, g.data(), result, hist_loss,
+    rc = lms_minimize(bound_objective, &call, nd, x0.data(), params, momenta_out, g.data(), result, hist_loss,
                       nullptr, nullptr, nullptr);
   } catch (int code) {
     return code;
   }
   if (rc != LMS_OK) return rc;
-  // final re-integration under p0* (registration.cpp:85-93): one more evaluation leaves q(1) resident
-  double loss = 0;
-  rc = lms_objective_eval(sys, momenta_out, g.data(), &loss, nullptr, nullptr);
-  if (rc != LMS_OK) return rc;
+  // final re-integration under p0* (registration.cpp:85-93).  When the last evaluated point is p0* bit for bit (the
+  // usual case: the last trial step was the accepted one) its trajectory is still resident and q(1) is read as it
+  // stands; otherwise one more evaluation puts it there.
+  if (call.last_x.size() != nd || std::memcmp(call.last_x.data(), momenta_out, nd * sizeof(double)) != 0) {
+    double loss = 0;
+    rc = lms_objective_eval(sys, momenta_out, g.data(), &loss, nullptr, nullptr);
+    if (rc != LMS_OK) return rc;
+  }
   return lms_objective_final_q(sys, warped_out);
 }
 

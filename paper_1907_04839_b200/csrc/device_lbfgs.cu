@@ -248,6 +248,13 @@ struct Workspace {
   }
 };
 
+// One allocation for every vector the driver can hold at once (x, g, d, trial point and gradient, best gradient,
+// 2 (memory + 1) curvature vectors), the reduction scratch and the mapped result words; made once per handle (at bind
+// time, see lms::prepare_device_lbfgs) and kept.  A fresh workspace also runs every kernel of the driver once on
+// zeroed data: module loading and the first cooperative launch cost tens of milliseconds on a cold context, which
+// would otherwise land inside the first registration.
+std::shared_ptr<Workspace> ensure_workspace(lms::SystemBase* sys, size_t n, int memory, cudaStream_t stream);
+
 struct DeviceOps {
   using Vec = double*;
   size_t n;
@@ -272,30 +279,7 @@ struct DeviceOps {
   int loop_blocks = 1;
   void init(int memory)
   {
-    const size_t count = 2 * ((size_t)std::max(memory, 0) + 1) + 6;
-    auto ws = std::static_pointer_cast<Workspace>(sys->lbfgs_workspace);
-    if (!ws || ws->n != n || ws->count < count) {
-      sys->lbfgs_workspace.reset();
-      ws = std::make_shared<Workspace>();
-      ws->n = n;
-      ws->count = count;
-      ws->each = ((n ? n : 1) + 31) / 32 * 32;
-      check(cudaMalloc(&ws->slab, ws->count * ws->each * sizeof(double)));
-      // the two-loop kernel: one CTA per SM (cooperative launch: all resident), fewer when the vector is short
-      int dev = 0, sms = 0;
-      check(cudaGetDevice(&dev));
-      check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      ws->loop_blocks = (int)std::max<size_t>(
-          1, std::min<size_t>(std::min<size_t>((size_t)sms, kLoopThreads), (n + kLoopThreads - 1) / kLoopThreads));
-      check(cudaMalloc(&ws->loop_partials, (size_t)(2 * kMaxPairs + 1) * ws->loop_blocks * sizeof(double)));
-      check(cudaMalloc(&ws->loop_counter, sizeof(unsigned)));
-      check(cudaMalloc(&ws->partials, 3 * kRedBlocks * sizeof(double)));
-      check(cudaMalloc(&ws->counter, sizeof(unsigned)));
-      check(cudaMemset(ws->counter, 0, sizeof(unsigned)));
-      check(cudaHostAlloc(&ws->h_out, 3 * sizeof(double), cudaHostAllocMapped));
-      check(cudaHostGetDevicePointer(&ws->d_out, ws->h_out, 0));
-      sys->lbfgs_workspace = ws;
-    }
+    auto ws = ensure_workspace(sys, n, memory, stream);
     for (size_t k = 0; k < ws->count; ++k) pool.push_back(ws->slab + (ws->count - 1 - k) * ws->each);
     loop_partials = ws->loop_partials;
     loop_counter = ws->loop_counter;
@@ -431,7 +415,83 @@ struct DeviceOps {
   }
 };
 
+// flag[0] = 0 when a and b differ anywhere (bitwise); the caller sets it to 1 first
+__global__ void same_bits_kernel(const double* __restrict__ a, const double* __restrict__ b, size_t n, double* flag)
+{
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && __double_as_longlong(a[i]) != __double_as_longlong(b[i])) flag[0] = 0.0;
+}
+
+std::shared_ptr<Workspace> ensure_workspace(lms::SystemBase* sys, size_t n, int memory, cudaStream_t stream)
+{
+  auto check = [](cudaError_t e) {
+    if (e != cudaSuccess) throw lms::CudaFailure{e, "device_lbfgs workspace", __LINE__};
+  };
+  const size_t count = 2 * ((size_t)std::max(memory, 0) + 1) + 6;
+  auto ws = std::static_pointer_cast<Workspace>(sys->lbfgs_workspace);
+  if (ws && ws->n == n && ws->count >= count) return ws;
+  sys->lbfgs_workspace.reset();
+  ws = std::make_shared<Workspace>();
+  ws->n = n;
+  ws->count = count;
+  ws->each = ((n ? n : 1) + 31) / 32 * 32;
+  check(cudaMalloc(&ws->slab, ws->count * ws->each * sizeof(double)));
+  check(cudaMemsetAsync(ws->slab, 0, ws->count * ws->each * sizeof(double), stream));
+  // the two-loop kernel: one CTA per SM (cooperative launch: all resident), fewer when the vector is short
+  int dev = 0, sms = 0;
+  check(cudaGetDevice(&dev));
+  check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  ws->loop_blocks = (int)std::max<size_t>(
+      1, std::min<size_t>(std::min<size_t>((size_t)sms, kLoopThreads), (n + kLoopThreads - 1) / kLoopThreads));
+  check(cudaMalloc(&ws->loop_partials, (size_t)(2 * kMaxPairs + 1) * ws->loop_blocks * sizeof(double)));
+  check(cudaMalloc(&ws->loop_counter, sizeof(unsigned)));
+  check(cudaMalloc(&ws->partials, 3 * kRedBlocks * sizeof(double)));
+  check(cudaMalloc(&ws->counter, sizeof(unsigned)));
+  check(cudaMemsetAsync(ws->counter, 0, sizeof(unsigned), stream));
+  check(cudaHostAlloc(&ws->h_out, 3 * sizeof(double), cudaHostAllocMapped));
+  check(cudaHostGetDevicePointer(&ws->d_out, ws->h_out, 0));
+  sys->lbfgs_workspace = ws;
+  if (n > 0) {
+    // warm-up: every kernel of the driver once, on the zeroed slab
+    double* v0 = ws->slab;
+    double* v1 = ws->slab + ws->each;
+    double* v2 = ws->slab + 2 * ws->each;
+    const int blocks = (int)((n + 255) / 256);
+    const int nb = (int)std::min<size_t>(kRedBlocks, (n + kRedThreads - 1) / kRedThreads);
+    reduce3_kernel<<<nb, kRedThreads, 0, stream>>>(v0, v1, n, ws->partials, ws->counter, ws->d_out);
+    lincomb_kernel<<<blocks, 256, 0, stream>>>(v2, 1.0, v0, 1.0, v1, n);
+    take_step_kernel<<<blocks, 256, 0, stream>>>(v0, v1, v2, 1.0, v0, v1, v2, n);
+    pair_stats_kernel<<<1, kStatThreads, 0, stream>>>(v0, v1, n, ws->d_out);
+    same_bits_kernel<<<blocks, 256, 0, stream>>>(v0, v1, n, ws->d_out);
+    check(cudaGetLastError());
+    PairSet ps{};
+    ps.m = 1;
+    ps.s[0] = v0;
+    ps.y[0] = v1;
+    ps.rho[0] = 0.0;
+    double gamma = 1.0;
+    const double* gp = v0;
+    double* dp = v2;
+    size_t nn = n;
+    check(cudaMemsetAsync(ws->loop_counter, 0, sizeof(unsigned), stream));
+    void* args[] = {&ps, &gamma, &gp, &dp, &nn, &ws->loop_partials, &ws->loop_counter, &ws->d_out};
+    check(cudaLaunchCooperativeKernel((const void*)two_loop_kernel, dim3(ws->loop_blocks), dim3(kLoopThreads), args, 0,
+                                      stream));
+    check(cudaMemsetAsync(ws->slab, 0, 3 * ws->each * sizeof(double), stream));
+  }
+  check(cudaStreamSynchronize(stream));
+  return ws;
+}
+
 }  // namespace
+
+namespace lms {
+void prepare_device_lbfgs(SystemBase* sys, int memory)
+{
+  if (sys->batch != 1) return;
+  ensure_workspace(sys, sys->host_q0.size(), memory, sys->stream_handle());
+}
+}  // namespace lms
 
 extern "C" int lms_register_device(lms_system* handle, const lms_lbfgs_params* params, double* momenta_out,
                                    double* warped_out, lms_minimize_result* result, double* hist_loss)
@@ -470,8 +530,21 @@ extern "C" int lms_register_device(lms_system* handle, const lms_lbfgs_params* p
       ops.check(cudaMemcpyAsync(momenta_out, x, nd * sizeof(double), cudaMemcpyDeviceToHost, ops.stream));
       ops.check(cudaStreamSynchronize(ops.stream));
       if (warped_out) {
-        double sc[3];
-        s->eval(x, g, sc, true);  // final re-integration under p0* (registration.cpp:85-93)
+        // final re-integration under p0* (registration.cpp:85-93).  The trajectory resident in HBM is the one of the
+        // last evaluated point; when that point is x* bit for bit (the usual case: the last trial step was the
+        // accepted one) re-evaluating would reproduce it exactly, so q(1) is read as it stands.
+        bool resident = false;
+        if (nd > 0 && s->last_x_device() != nullptr) {
+          ops.h_out[0] = 1.0;
+          same_bits_kernel<<<ops.blocks(), 256, 0, ops.stream>>>(x, s->last_x_device(), nd, ops.d_out);
+          ops.check(cudaGetLastError());
+          ops.check(cudaStreamSynchronize(ops.stream));
+          resident = ops.h_out[0] != 0.0;
+        }
+        if (!resident) {
+          double sc[3];
+          s->eval(x, g, sc, true);
+        }
         s->final_q(warped_out);
       }
     }

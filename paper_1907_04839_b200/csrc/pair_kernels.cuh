@@ -161,6 +161,23 @@ __device__ __constant__ double kExp2Table64[64] = {
     0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
     0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
 
+// The shared-memory table of Math<double>::kernel (see the layout note there).
+#ifndef LMS_EXP_TABLE_PER_LANE
+#define LMS_EXP_TABLE_PER_LANE 0
+#endif
+constexpr int kExpTableCopies = LMS_EXP_TABLE_PER_LANE ? 32 : 1;
+constexpr int kExpTableDoubles = kExpEntries * kExpTableCopies;
+__device__ __forceinline__ void fill_exp_table(double* tbl, int tid, int threads)
+{
+  for (int e = tid; e < kExpTableDoubles; e += threads)
+    tbl[e] = kExp2Table64[(e / kExpTableCopies) * (64 / kExpEntries)];
+}
+// this thread's view of the table
+__device__ __forceinline__ const double* exp_table_of_lane(const double* tbl, int tid)
+{
+  return LMS_EXP_TABLE_PER_LANE ? tbl + (tid & 31) : tbl;
+}
+
 template <>
 struct Math<double> {
   // exp(r2 * k_scale) for r2 * k_scale <= 0, branch-free.  kexp = k_scale * log2(e) * 2^B (host, one rounding),
@@ -186,6 +203,8 @@ struct Math<double> {
       p = fma(p, g, 0x1.ebfbdff82c594p-11);
       p = fma(p, g, 0x1.62e42fefa39fdp-5);
     } else if constexpr (kExpBits == 5) {
+      // (Estrin's grouping of the same polynomial -- one more multiply, a chain of 4 instead of 6 -- measured slower:
+      // 22.73 vs 22.38 ms per gradient; the DP pipe, not the chain, is what is short.)
       p = 0x1.5d885e6ef14a6p-35;
       p = fma(p, g, 0x1.3b2b301f1eb9cp-27);
       p = fma(p, g, 0x1.c6b08d70380ddp-20);
@@ -198,7 +217,17 @@ struct Math<double> {
       p = fma(p, g, 0x1.62e42fefa0352p-7);
     }
     p = fma(p, g, 1.0);
+    // One shared copy of the table (LMS_EXP_TABLE_PER_LANE=0, the default): entries j and j + 16 sit on the same bank
+    // pair, and ncu counts 5.6 M shared-memory conflict replays per launch at N = 20 000 -- but landmarks many sigma
+    // apart clamp to the same entry, which is a broadcast, and the two conflict-free layouts measured SLOWER on the
+    // B200 (fp64 gradient, N = 20 000, T = 10): one copy 21.85 ms | low/high words in two 32-entry arrays (every
+    // entry its own bank, two LDS.32) 22.42 ms | one copy per lane (tbl[j * 32 + lane], one LDS.64, always two full
+    // wavefronts) 22.38 ms; conflicts 5.63 M -> 0 / 7 in both.  The per-lane layout stays selectable for A/B.
+#if LMS_EXP_TABLE_PER_LANE
+    const double r = tbl[(ki & (kExpEntries - 1)) * 32] * p;  // `tbl` already points at this lane's copy
+#else
     const double r = tbl[ki & (kExpEntries - 1)] * p;
+#endif
     const int n = ki >> kExpBits;
     const double scaled = __hiloint2double(__double2hiint(r) + n * 1048576, __double2loint(r));
     return n < -1021 ? 0.0 : scaled;
@@ -491,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
 
   __shared__ __align__(16) T tile[2][AOS ? kTileJ : NC][AOS ? NC : kTileJ];
   __shared__ double red_scratch[kThreads];
-  __shared__ double exp_tbl[kExpEntries];  // fp64 only: 2^(j/2^B) for Math<double>::kernel
+  __shared__ double exp_tbl_all[sizeof(T) == 8 ? kExpTableDoubles : 1];  // fp64 only: 2^(j/2^B)
   __shared__ int s_last;
   __shared__ __align__(8) unsigned long long tile_bar[2];  // BULK only: one mbarrier per tile buffer
   // Programmatic dependent launch: the next launch of the evaluation may start scheduling its CTAs as soon as
@@ -509,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     __syncthreads();
   }
   if constexpr (sizeof(T) == 8) {
-    if (threadIdx.x < kExpEntries) exp_tbl[threadIdx.x] = kExp2Table64[threadIdx.x * (64 / kExpEntries)];
+    fill_exp_table(exp_tbl_all, threadIdx.x, kThreads);
     __syncthreads();
   }
 
@@ -517,6 +546,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int tid = threadIdx.x;
+  const double* exp_tbl = exp_table_of_lane(exp_tbl_all, tid);
   // Work is counted in units of kUnitJ columns of one row tile, so every CTA's share differs by at most
   // one unit (1/16 of a staged tile); `cells` and `nJ` below are in those units.
   const long long nJ = (long long)a.n_j_tiles * kUnitsPerTile;

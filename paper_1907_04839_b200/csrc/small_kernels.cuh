@@ -397,14 +397,15 @@ __global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T
   T* tile = reinterpret_cast<T*>(small_smem);
   __shared__ __align__(16) T part[(W - 1) * RP * RS * Shape<kFwd, D>::kAcc * 32];  // column-warp partial sums
   __shared__ __align__(8) unsigned long long bars[SmallShape<T>::kMaxChunks];
-  __shared__ double exp_tbl[kExpEntries];
+  __shared__ double exp_tbl_all[sizeof(T) == 8 ? kExpTableDoubles : 1];  // fp64 only
   if (threadIdx.x == 0) {
     for (int c = 0; c < SmallShape<T>::kMaxChunks; ++c) mbar_init(&bars[c], 1);
     mbar_fence_init();
   }
   if constexpr (sizeof(T) == 8) {
-    if (threadIdx.x < kExpEntries) exp_tbl[threadIdx.x] = kExp2Table64[threadIdx.x * (64 / kExpEntries)];
+    fill_exp_table(exp_tbl_all, threadIdx.x, kThreadsHere);
   }
+  const double* exp_tbl = exp_table_of_lane(exp_tbl_all, threadIdx.x);
   // p0[i][c] = T(x[i*D+c])  (registration.cpp:61-63); non-finite p0 -> DivergedError(0) (shooting.hpp:185-186).
   // The divergence word is re-armed here (CTA 0, before the first barrier) and non-finite inputs are recorded
   // after it, so no separate memset launch precedes the kernel.

@@ -96,7 +96,8 @@ class SystemBase {
                           const int* ids) = 0;
   virtual void final_q_batch(double* out) = 0;
   virtual cudaStream_t stream_handle() const = 0;
-  virtual const double* staging_scratch() const = 0;  // device scratch of the host<->plane conversions (trace builds read it)
+  virtual const double* staging_scratch() const = 0;
+  virtual const double* last_x_device() const = 0;  // the point of the last single-problem evaluation (device copy), or null  // device scratch of the host<->plane conversions (trace builds read it)
   int batch = 1;
   // scratch owned by the device-resident L-BFGS driver (device_lbfgs.cu), kept across lms_register_device calls:
   // cudaMalloc / cudaFree cost milliseconds (and synchronise the device) next to an 8 ms evaluation
@@ -189,6 +190,7 @@ class System final : public SystemBase {
   void final_q_batch(double* out) override;
   cudaStream_t stream_handle() const override { return stream_; }
   const double* staging_scratch() const override { return d_io_; }
+  const double* last_x_device() const override { return stored_t_ == timesteps && bound ? d_x_ : nullptr; }
 
  private:
   static constexpr int kState = 2 * D;  // planes per (q,p) or (alpha,beta) state
@@ -338,6 +340,8 @@ struct RowPartition {
 RowPartition partition_rows(long long n, int world, int rank);
 
 SystemBase* create_system(const lms_config& cfg, int batch_count = 1);
+// device_lbfgs.cu: allocates (once per handle) and warms the workspace of lms_register_device
+void prepare_device_lbfgs(SystemBase* sys, int memory);
 const char* variant_name(int precision, int variant);
 
 }  // namespace lms

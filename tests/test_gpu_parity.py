@@ -907,7 +907,9 @@ def test_result_document_of_a_registration_reproduces_the_warp(tmp_path):
     s = HamiltonianSystem(doc.config.sigma, n, 3, doc.config.precision, max_timesteps=doc.config.timesteps)
     tq, _ = s.integrate_forward(doc.template, doc.momenta.reshape(n, 3), doc.config.timesteps)
     s.close()
-    assert np.array_equal(tq[-1], doc.warped)  # same kernels, same inputs: bit for bit
+    # same inputs through the per-function path (tiled kernels; the registration itself ran the persistent kernel):
+    # equal to rounding
+    assert rel_inf(tq[-1], doc.warped) <= 1e-12
     assert doc.avg_after < doc.avg_before
 
 
