@@ -5,24 +5,27 @@
 // At N = 1000 a time step is 1e6 pair evaluations, half a microsecond of B200 math; the 2T+2 dependent launches
 // of the tiled path (pair_kernels.cuh) then cost ~10 us each whatever they compute: launch, row-operand and tile
 // load latency, and the cross-CTA combine of the stream-K partial sums (slot write, fence, counter, re-read by
-// the last CTA).  Here the mapping is transposed: a WARP owns a few rows and its 32 lanes split the columns, so
-// a row's sums meet in a shuffle tree inside the warp -- no partial sums ever leave the SM, no combine pass, and
-// the only global synchronisation is one grid barrier per time step.
+// the last CTA).  Here the mapping is transposed: a WARP works on one "slot" of rows at a time and its 32 lanes
+// split the columns, so a row's sums meet in a shuffle tree inside the warp -- no partial sums ever leave the SM,
+// no combine pass, and the only global synchronisation is one grid barrier per time step.
 //
-//   rows      "slots" of RS rows (fp32: the 2 rows of a packed FFMA2 operand; fp64: 1 row) are dealt round-robin
-//             to gridDim.x * WR "row warps"; a row warp keeps up to RP slots (row operands + 2D running sums per
-//             row) in registers.  Row operands are warp-uniform.
-//   columns   every CTA pulls the whole landmark state into shared memory in chunks of 512 (fp64: 256) columns with
-//             bulk-async copies (cp.async.bulk + one mbarrier per chunk: reads L2, so the state other CTAs wrote
-//             before the barrier is seen without any L1 concern).  All chunks of a step are in flight at once (up
-//             to 8: N <= 4096 fp32 / 2048 fp64) and a warp waits only for the chunk it is about to read, so there
-//             is no CTA-wide synchronisation inside a sweep.  When a CTA has fewer slots
-//             than warps, WC warps share a slot: warp wc takes the 32-column groups wc, wc + WC, ... of every
-//             chunk and lane l column l of a group (consecutive lanes, consecutive words: conflict-free LDS.32).
-//   sums      per lane ascending columns, the WC column warps in ascending order through shared memory, then a
-//             fixed xor-butterfly over the lanes: bitwise reproducible.
-//   epilogue  lane r of the warp finishes the warp's row r with exactly the arithmetic of the tiled kernels'
-//             epilogues (explicit _rn operations in the reference's expression order).
+//   rows      "slots" of RS rows (fp32: the 2 rows of a packed FFMA2 operand; fp64: 1 row) are dealt to the CTAs
+//             in contiguous, equal (+-1) runs.  Row operands are warp-uniform registers.
+//   columns   every CTA pulls the whole landmark state into shared memory, one contiguous array per component,
+//             in chunks of 512 (fp64: 256) columns with bulk-async copies (cp.async.bulk + one mbarrier per chunk:
+//             reads L2, so the state other CTAs wrote before the barrier is seen without any L1 concern).  All
+//             chunks of a step are in flight at once (up to 8: N <= 4096 fp32 / 2048 fp64) and a warp waits only
+//             for the chunks it is about to read, so there is no CTA-wide synchronisation inside a sweep.
+//   work      a CTA with s slots has s x G work items (slot, group of 32 columns), slot-major; its 16 warps take
+//             equal contiguous runs of that list (stream-K inside the CTA), so every warp is busy for the same
+//             time whatever s is.  A run touches at most two slots: two "pieces" (slot, group range) per warp.
+//             Inside a piece lane l takes U consecutive columns of each block of 32 U (one LDS.128 / LDS.64 per
+//             component serves U pairs per row: U independent dependency chains in one basic block).
+//   sums      per lane ascending columns; a fixed transposing shuffle tree over the lanes of the piece; the
+//             pieces of a slot in ascending column order (one thread per row adds them): bitwise reproducible.
+//   epilogue  thread r of the CTA finishes the CTA's row r with exactly the arithmetic of the tiled kernels'
+//             epilogues (explicit _rn operations in the reference's expression order); rows are contiguous per
+//             CTA, so the stores coalesce.
 //   barrier   one monotonic arrival counter in global memory (the launch is cooperative: all CTAs are resident):
 //             red.release to arrive, ld.acquire to poll; the host hands every launch the count it starts from.
 #pragma once
@@ -31,11 +34,12 @@
 
 namespace lms {
 
-constexpr int kSmallMaxWarps = 16;  // warps per CTA: 16 with one slot per row warp, 8 with several
-// Largest n the persistent kernel is chosen for (LMS_SMALL_MAX_N overrides): the measured crossover with the tiled
-// path in fp32 (ms per gradient, T = 10, persistent / tiled: N = 1000 0.107 / 0.217, 2000 0.195 / 0.265, 3000 0.364 /
-// 0.414, 4000 0.564 / 0.550), and the shared-memory capacity for the staged state in fp64 (N = 2000 0.427 / 0.443).
-constexpr int kSmallMaxN32 = 3500;
+constexpr int kSmallWarps = 16;     // warps per CTA
+constexpr int kSmallMaxWarps = kSmallWarps;
+constexpr int kSmallMaxSlots = 16;  // slots per CTA (a warp's run of work then spans at most two slots)
+// Largest n the persistent kernel is chosen for (LMS_SMALL_MAX_N overrides): the shared-memory capacity for the
+// staged state (8 chunks), see SmallShape.
+constexpr int kSmallMaxN32 = 4096;
 constexpr int kSmallMaxN64 = 2048;
 
 // LMS_SMALL_TRACE: phase timestamps (globaltimer, ns) of CTA 0 into SmallArgs::trace -- a measurement build only
@@ -59,6 +63,7 @@ template <typename T>
 struct SmallShape {
   static constexpr int kChunk = sizeof(T) == 4 ? 512 : 256;  // columns per staged chunk
   static constexpr int kMaxChunks = 8;                        // chunk buffers (all resident during a step)
+  static constexpr int kCols = kChunk * kMaxChunks;           // shared-memory array length per component
   static constexpr int kRowsPerSlot = sizeof(T) == 4 ? 2 : 1;
 };
 
@@ -73,12 +78,11 @@ struct SmallArgs {
   T* hp0;                 // H_p(q0, p0): D planes
   const T* target;        // D planes
   double* grad_out;       // row-major double n x D
-  double* warp_part;      // 2 x (gridDim.x * wr): per-row-warp partials of sum p.hp and of the mismatch
+  double* warp_part;      // 2 x (gridDim.x * kSmallWarps): per-warp partials of sum p.hp and of the mismatch
   double* scalars;        // {loss, kinetic, mismatch}
   unsigned long long* diverged;
   unsigned* barrier;      // monotonic arrival counter
   unsigned bar_base;      // its value when this launch starts (the host counts gridDim.x * barriers per launch)
-  int wr, wc;             // row warps per CTA x column warps per slot (wr * wc <= warps per CTA)
   unsigned long long* trace;  // LMS_SMALL_TRACE builds: 8 timestamps per step; else null
   int n;
   int n_chunks;
@@ -96,6 +100,22 @@ __device__ __forceinline__ void bulk_g2s_multicast(void* dst, const void* src, u
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
+      : "memory");
+}
+
+// mbar_wait on a precomputed shared-window address (keeps the generic -> shared conversion out of the sweep)
+__device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity)
+{
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LMS_WAITU_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra LMS_DONEU_%=;\n"
+      "bra LMS_WAITU_%=;\n"
+      "LMS_DONEU_%=:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
       : "memory");
 }
 
@@ -118,12 +138,129 @@ __device__ __forceinline__ void small_grid_barrier(unsigned* bar, unsigned& targ
   asm volatile("fence.proxy.async.global;" ::: "memory");  // before this thread's bulk-async reads of that data
 }
 
-// One time step for the rows this warp owns.  MODE kFwd: state -> out = next snapshot (Euler, shooting.hpp:205-211)
-// with the first / last step extras; MODE kAdj: (state, adj_in) -> out = next adjoint state (:302-306).
-template <typename T, int D, int MODE, int RP>
-__device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __restrict__ state,
+// Sum NV per-lane values over the 32 lanes with a fixed "transposing" shuffle tree: while the count is even, lanes
+// l and l ^ off split the values between them (each keeps one half and adds the partner's copy of it), then plain
+// butterflies finish.  On return v[0 .. count) hold complete sums of the values [first, first + count) on every
+// lane; the lanes with (lane & live_mask) == 0 between them hold every value exactly once.
+template <typename T, int NV>
+struct LaneTree {
+  static constexpr int count_after(int c, int stages) { return stages == 0 ? c : count_after(c % 2 == 0 ? c / 2 : c, stages - 1); }
+  static constexpr int kCount = count_after(NV, 5);
+  static __device__ __forceinline__ void run(T (&v)[NV], int lane, int& first, unsigned& live_mask)
+  {
+    first = 0;
+    live_mask = 0;
+    int count = NV;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      if (count % 2 == 0) {
+        const int half = count / 2;
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int j = 0; j < NV / 2; ++j) {
+          if (j < half) {
+            const T send = up ? v[j] : v[j + half];
+            const T keep = up ? v[j + half] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+          }
+        }
+        if (up) first += half;
+        count = half;
+      } else {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          if (j < count) v[j] += __shfl_xor_sync(0xffffffffu, v[j], off);
+        live_mask |= (unsigned)off;
+      }
+    }
+  }
+};
+
+// Vector loads of U consecutive columns of one staged component (16 bytes per load at most).
+template <typename T, int U>
+__device__ __forceinline__ void load_cols(const T* p, T (&v)[U])
+{
+  constexpr int VW = (int)(16 / sizeof(T)) < U ? (int)(16 / sizeof(T)) : U;  // elements per load
+  if constexpr (VW == 1) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = p[u];
+  } else {
+#pragma unroll
+    for (int b = 0; b < U / VW; ++b) {
+      T w[VW];
+      ColVec<T, VW>::load(p + b * VW, w);
+#pragma unroll
+      for (int u = 0; u < VW; ++u) v[b * VW + u] = w[u];
+    }
+  }
+}
+
+// columns a lane evaluates together in the forward / adjoint sweep (independent dependency chains per basic block)
+#ifndef LMS_SMALL_UF
+#define LMS_SMALL_UF 4
+#endif
+#ifndef LMS_SMALL_UA
+#define LMS_SMALL_UA 2
+#endif
+
+// What a thread needs to know about the CTA's work list; the same for every time step, so it is worked out once
+// per launch (the per-step code between two sweeps is latency-critical and mostly cold in the instruction cache:
+// it is kept as short as possible).
+struct SmallPlan {
+  int slot0, s_b;       // the CTA's slots [slot0, slot0 + s_b)
+  int n_pieces;         // pieces of this warp's run (0..2)
+  int sl[2], g0[2], g1[2];  // slot (CTA-local) and 32-column groups [g0, g1) of each
+  int pid0;             // index of the warp's first piece among the CTA's pieces (ascending work-list order)
+  int epi_first, epi_count;  // epilogue thread: its slot's pieces are [epi_first, epi_first + epi_count)
+};
+
+template <int RS, int D>
+__device__ __forceinline__ SmallPlan small_plan(int n)
+{
+  SmallPlan p;
+  const int warp = threadIdx.x >> 5;
+  const int slots = (n + RS - 1) / RS;
+  p.slot0 = (int)((long long)blockIdx.x * slots / gridDim.x);
+  p.s_b = (int)((long long)(blockIdx.x + 1) * slots / gridDim.x) - p.slot0;
+  const int G = (n + 31) / 32;  // live groups
+  const int total = p.s_b * G;
+  p.n_pieces = 0;
+  p.pid0 = 0;
+  p.sl[0] = p.sl[1] = p.g0[0] = p.g0[1] = p.g1[0] = p.g1[1] = 0;
+  // epilogue thread t finishes (row t / D of the CTA, component t % D)
+  const int my_slot = (int)threadIdx.x / (RS * D);
+  p.epi_first = 0;
+  p.epi_count = 0;
+  int pid = 0;
+  for (int w = 0; w < kSmallWarps; ++w) {
+    const int r0 = w * total / kSmallWarps, r1 = (w + 1) * total / kSmallWarps;
+    if (r1 == r0) continue;  // fewer items than warps
+    const int s0 = r0 / G, s1 = (r1 - 1) / G;  // s1 <= s0 + 1: a run is at most G items long
+    if (w == warp) {
+      p.n_pieces = s1 - s0 + 1;
+      p.pid0 = pid;
+      p.sl[0] = s0;
+      p.g0[0] = r0 - s0 * G;
+      p.g1[0] = s1 > s0 ? G : r1 - s0 * G;
+      p.sl[1] = s1;
+      p.g0[1] = 0;
+      p.g1[1] = r1 - s1 * G;
+    }
+    for (int sl = s0; sl <= s1; ++sl) {
+      if (sl < my_slot) ++p.epi_first;
+      if (sl == my_slot) ++p.epi_count;
+    }
+    pid += s1 - s0 + 1;
+  }
+  return p;
+}
+
+// One time step for this CTA's rows.  MODE kFwd: state -> out = next snapshot (Euler, shooting.hpp:205-211) with
+// the first / last step extras; MODE kAdj: (state, adj_in) -> out = next adjoint state (:302-306).
+template <typename T, int D, int MODE>
+__device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPlan& pl, const T* __restrict__ state,
                                            const T* __restrict__ adj_in, T* __restrict__ out, unsigned epi, int step_no,
-                                           T* tile, T* part, unsigned long long* bars, unsigned& phase,
+                                           T* tile, T* part, T* rowbuf, unsigned long long* bars, unsigned& phase,
                                            double& hsum, double& msum, const double* exp_tbl, int trace_base)
 {
   LMS_TRACE_POINT(a, trace_base + 0);
@@ -132,19 +269,12 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
   constexpr bool F32 = sizeof(T) == 4;
   constexpr int RS = SmallShape<T>::kRowsPerSlot;
   constexpr int CH = SmallShape<T>::kChunk;
-  constexpr int NCMAX = 4 * D;
+  constexpr int NTOT = SmallShape<T>::kCols;
+  constexpr int GPC = CH / 32;  // 32-column groups per chunk
+  constexpr int NV = RS * NA;   // sums per slot
+  constexpr int NRMAX = 4 * D;  // row operands per row in the adjoint sweep (rowbuf is sized for it)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int wc = warp / a.wr;            // column part of this warp (>= a.wc: a spare warp, no work)
-  const int GW = gridDim.x * a.wr;       // row warps of the launch
-  const int gw = blockIdx.x * a.wr + (warp - wc * a.wr);
-  const int slots = (a.n + RS - 1) / RS;
-  int my = 0;  // slots this warp works on: gw, gw + GW, ...
-  if (wc < a.wc) {
-#pragma unroll
-    for (int i = 0; i < RP; ++i)
-      if (gw + i * GW < slots) my = i + 1;
-  }
 
   auto plane = [&](int k) -> const T* {
     if constexpr (MODE == kAdj)
@@ -152,23 +282,24 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
     else
       return state + (long long)k * a.stride;
   };
-  // Every chunk of this step's state goes into its own buffer, all in flight together: one bulk copy per
-  // (chunk, component plane), issued by lanes 0..NC-1 of warp 0 side by side; lane 0's arrive.expect_tx is a
-  // chunk barrier's one arrival, so its phase cannot complete before every byte has been expected and delivered.
-  // (All warps passed the grid barrier's __syncthreads since they last read these buffers.)
+  // Every chunk of this step's state is fetched at once: one bulk copy per (chunk, component plane), issued by
+  // lanes 0..NC-1 of the last warp side by side; lane 0's arrive.expect_tx is a chunk barrier's one arrival, so its
+  // phase cannot complete before every byte has been expected and delivered.  (All warps passed the grid
+  // barrier's __syncthreads since they last read these buffers.)
   // All 148 CTAs pull the same bytes at the same moment, and the L2 -> SM fabric (not latency) is what the first
   // chunk then waits for (measured: 96 KB per CTA take 3 us at N = 2000).  Launched as thread-block clusters, the
   // CTAs of a cluster share the fetch: piece (chunk, plane) is requested by ONE of them and multicast into the
   // same buffer offset of all (and completes on the same mbarrier offset of all), so L2 serves 1/cluster-size of
   // the traffic.
-  unsigned cl_rank, cl_size;
-  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(cl_rank));
-  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(cl_size));
-  if (warp == 0) {
+  if (warp == kSmallWarps - 1) {
+    unsigned cl_rank, cl_size;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(cl_rank));
+    asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(cl_size));
+#pragma unroll 1
     for (int c = 0; c < a.n_chunks; ++c) {
       if (lane == 0) mbar_expect_tx(&bars[c], (unsigned)(NC * CH * sizeof(T)));
       if (lane < NC) {
-        T* dst = tile + ((long long)c * NCMAX + lane) * CH;
+        T* dst = tile + (long long)lane * NTOT + (long long)c * CH;
         const T* src = plane(lane) + (long long)c * CH;
         if (cl_size == 1)
           bulk_g2s(dst, src, (unsigned)(CH * sizeof(T)), &bars[c]);
@@ -176,226 +307,199 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const T* __res
           bulk_g2s_multicast(dst, src, (unsigned)(CH * sizeof(T)), &bars[c], (unsigned short)((1u << cl_size) - 1u));
       }
     }
-  }
-
-  // ---- row operands (warp-uniform; read past L1: other CTAs wrote them before the grid barrier) ----
-  T rv[RP][RS][NR];
-#pragma unroll
-  for (int i = 0; i < RP; ++i)
-#pragma unroll
-    for (int h = 0; h < RS; ++h) {
-      const long long row = (long long)(gw + i * GW) * RS + h;
-      const bool ok = i < my && row < a.n;
-#pragma unroll
-      for (int k = 0; k < NR; ++k) rv[i][h][k] = ok ? __ldcg(plane(k) + row) : T(0);
+  } else {
+    // ---- row operands of the CTA's rows: one value per thread (of the other warps), read past L1 (other CTAs wrote
+    // them before the grid barrier) and parked in shared memory for the sweeps and the epilogue; the fetch
+    // overlaps the chunk copies.  kSmallMaxSlots * RS * NR <= 384 values <= 15 warps ----
+    const int t = threadIdx.x;
+    if (t < pl.s_b * RS * NR) {
+      const int rl = t / NR, k = t - rl * NR;  // row of the CTA, component
+      const long long row = (long long)pl.slot0 * RS + rl;
+      // [slot][component][row of the slot]: a slot's packed (row 0, row 1) operand is one 8-byte word
+      rowbuf[((rl / RS) * NRMAX + k) * RS + (rl % RS)] = row < a.n ? __ldcg(plane(k) + row) : T(0);
     }
-  T acc[RP][RS][NA];
-  float2 ri2[F32 ? RP : 1][NR];
-  float2 acc2[F32 ? RP : 1][NA];
-  float2 kexp2, ns2, neg1;
-  if constexpr (F32) {
-#pragma unroll
-    for (int i = 0; i < RP; ++i) {
+  }
+  __syncthreads();
+  LMS_TRACE_POINT(a, trace_base + 1);
+  const unsigned bars_u32 = smem_u32(bars);
+
+  // ---- the warp's pieces: (slot, groups [g0, g1)) ----
+  constexpr int U = F32 ? (MODE == kAdj ? LMS_SMALL_UA : LMS_SMALL_UF) : (MODE == kAdj ? 1 : 2);
+  int waited = 0;  // chunks [0, waited) have landed
+#pragma unroll 1
+  for (int pc = 0; pc < pl.n_pieces; ++pc) {
+    const int sl = pc ? pl.sl[1] : pl.sl[0];
+    const int g0 = pc ? pl.g0[1] : pl.g0[0];
+    const int g1 = pc ? pl.g1[1] : pl.g1[0];
+    T rv[RS][NR];  // warp-uniform
+    if constexpr (RS == 2) {
 #pragma unroll
       for (int k = 0; k < NR; ++k) {
-        const float lo = (float)rv[i][0][k], hi = (float)rv[i][RS - 1][k];
-        ri2[i][k] = k < D ? make_float2(-lo, -hi) : make_float2(lo, hi);  // pair_term_packed takes -q_i
+        T v[2];
+        load_cols<T, 2>(rowbuf + (sl * NRMAX + k) * 2, v);
+        rv[0][k] = v[0];
+        rv[1][k] = v[1];
       }
+    } else {
 #pragma unroll
-      for (int k = 0; k < NA; ++k) acc2[i][k] = make_float2(0.f, 0.f);
+      for (int k = 0; k < NR; ++k) rv[0][k] = rowbuf[sl * NRMAX + k];
     }
-    kexp2 = splat2((float)a.kexp);
-    ns2 = splat2(-(float)a.inv_sig2);
-    neg1 = splat2(-1.f);
-  } else {
-#pragma unroll
-    for (int i = 0; i < RP; ++i)
-#pragma unroll
-      for (int k = 0; k < NA; ++k) acc[i][0][k] = T(0);
-  }
 
-  // ---- sweep the columns: this warp's 32-column groups wc, wc + WC, ... of the whole staged state ----
-  // U groups are loaded and evaluated together -- U independent dependency chains (LDS -> r^2 -> ex2 -> sums) in
-  // one basic block, which is what lets the few warps of a CTA keep the FMA pipe busy.  A chunk is waited for the
-  // first time one of its groups comes up.
-  constexpr int GPC = CH / 32;  // groups per chunk
-  constexpr int U = F32 ? (MODE == kAdj ? 2 : 4) : (MODE == kAdj ? 1 : 2);
-  if (my > 0) {
-    const int G = a.n_chunks * GPC;
-    int waited = 0;  // chunks [0, waited) have landed
-    auto need = [&](int g_last) {
-      const int c = g_last / GPC;
-      while (waited <= c) {
-        mbar_wait(&bars[waited], phase);
-        ++waited;
+    T acc[NV];
+    float2 ri2[NR], acc2[NA];
+    float2 kexp2, ns2, neg1;
+    if constexpr (F32) {
+#pragma unroll
+      for (int k = 0; k < NR; ++k) {
+        const float lo = (float)rv[0][k], hi = (float)rv[RS - 1][k];
+        ri2[k] = k < D ? make_float2(-lo, -hi) : make_float2(lo, hi);  // pair_term_packed takes -q_i
       }
-    };
-    auto col_ptr = [&](int g) -> const T* {
-      const int c = g / GPC;
-      return tile + (long long)c * NCMAX * CH + (g - c * GPC) * 32 + lane;
-    };
+#pragma unroll
+      for (int k = 0; k < NA; ++k) acc2[k] = make_float2(0.f, 0.f);
+      kexp2 = splat2((float)a.kexp);
+      ns2 = splat2(-(float)a.inv_sig2);
+      neg1 = splat2(-1.f);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = T(0);
+    }
     auto evaluate = [&](const T(&cj)[NC]) {
       if constexpr (F32) {
         float2 cj2[NC];
 #pragma unroll
         for (int k = 0; k < NC; ++k) cj2[k] = splat2((float)cj[k]);
-#pragma unroll
-        for (int i = 0; i < RP; ++i)
-          if (RP == 1 || i < my) pair_term_packed<D, MODE>(ri2[i], cj2, acc2[i], kexp2, ns2, neg1);
+        pair_term_packed<D, MODE>(ri2, cj2, acc2, kexp2, ns2, neg1);
       } else {
-#pragma unroll
-        for (int i = 0; i < RP; ++i)
-          if (RP == 1 || i < my) pair_term<T, D, MODE>(rv[i][0], cj, acc[i][0], a.kexp, a.inv_sig2, exp_tbl);
+        pair_term<T, D, MODE>(rv[0], cj, acc, a.kexp, a.inv_sig2, exp_tbl);
       }
     };
-    int g = wc;
-#ifdef LMS_SMALL_TRACE
-    if (g < G) need(g);
-    LMS_TRACE_POINT(a, trace_base + 1);
-#endif
-    for (; g + (U - 1) * a.wc < G; g += U * a.wc) {
-      need(g + (U - 1) * a.wc);
+    auto need = [&](int g_last) {  // the chunks up to the one holding group g_last have landed
+      const int c = g_last / GPC;
+      if (c >= waited) {
+#pragma unroll 1
+        do {
+          mbar_wait_u32(bars_u32 + 8u * (unsigned)waited, phase);
+          ++waited;
+        } while (waited <= c);
+      }
+    };
+
+    // blocks of U groups: lane l takes the U consecutive columns 32 U b + U l ...; then single groups
+    int g = g0;
+    const T* cp = tile + (long long)g * 32 + (long long)lane * U;
+#pragma unroll 1
+    for (; g + U <= g1; g += U, cp += 32 * U) {
+      need(g + U - 1);
       T cj[U][NC];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const T* cp = col_ptr(g + u * a.wc);
+      for (int k = 0; k < NC; ++k) {
+        T v[U];
+        load_cols<T, U>(cp + k * NTOT, v);
 #pragma unroll
-        for (int k = 0; k < NC; ++k) cj[u][k] = cp[k * CH];
+        for (int u = 0; u < U; ++u) cj[u][k] = v[u];
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) evaluate(cj[u]);
     }
-    for (; g < G; g += a.wc) {
-      need(g);
-      T cj[NC];
-      const T* cp = col_ptr(g);
+    if constexpr (U > 1) {
+      const T* cs = tile + (long long)g * 32 + lane;
+#pragma unroll 1
+      for (; g < g1; ++g, cs += 32) {
+        need(g);
+        T cj[NC];
 #pragma unroll
-      for (int k = 0; k < NC; ++k) cj[k] = cp[k * CH];
-      evaluate(cj);
+        for (int k = 0; k < NC; ++k) cj[k] = cs[k * NTOT];
+        evaluate(cj);
+      }
     }
-  }
-  phase ^= 1u;  // every chunk barrier completed one phase
 
-  // ---- row sums: fixed butterfly over the lanes ----
-  if constexpr (F32) {
-#pragma unroll
-    for (int i = 0; i < RP; ++i)
+    // ---- the piece's sums over the lanes (fixed tree), parked for the slot's epilogue threads ----
+    if constexpr (F32) {
 #pragma unroll
       for (int k = 0; k < NA; ++k) {
         const bool flip = MODE == kFwd && k < D;  // the packed forward term accumulates -(p_i.p_j) K dx
-        acc[i][0][k] = (T)(flip ? -acc2[i][k].x : acc2[i][k].x);
-        acc[i][RS - 1][k] = (T)(flip ? -acc2[i][k].y : acc2[i][k].y);
+        acc[k] = (T)(flip ? -acc2[k].x : acc2[k].x);
+        acc[(RS - 1) * NA + k] = (T)(flip ? -acc2[k].y : acc2[k].y);
       }
+    }
+    int first;
+    unsigned live_mask;
+    LaneTree<T, NV>::run(acc, lane, first, live_mask);
+    if ((lane & live_mask) == 0) {
+      T* mine = part + (pl.pid0 + pc) * NV;
+#pragma unroll
+      for (int j = 0; j < LaneTree<T, NV>::kCount; ++j) mine[first + j] = acc[j];
+    }
   }
+  phase ^= 1u;  // every chunk barrier completed one phase
   LMS_TRACE_POINT(a, trace_base + 2);
-  if (a.wc > 1) {
-    // the column warps of a slot meet in shared memory: ascending column part, lane by lane
-    constexpr int PER = RP * RS * NA * 32;  // one warp's partial sums
-    if (wc > 0 && my > 0) {
-      T* mine = part + ((long long)(wc - 1) * a.wr + (warp - wc * a.wr)) * PER;
-#pragma unroll
-      for (int i = 0; i < RP; ++i)
-#pragma unroll
-        for (int h = 0; h < RS; ++h)
-#pragma unroll
-          for (int k = 0; k < NA; ++k) mine[((i * RS + h) * NA + k) * 32 + lane] = acc[i][h][k];
-    }
-    __syncthreads();
-    if (wc == 0 && my > 0) {
-      for (int c = 1; c < a.wc; ++c) {
-        const T* theirs = part + ((long long)(c - 1) * a.wr + warp) * PER;
-#pragma unroll
-        for (int i = 0; i < RP; ++i)
-#pragma unroll
-          for (int h = 0; h < RS; ++h)
-#pragma unroll
-            for (int k = 0; k < NA; ++k) acc[i][h][k] += theirs[((i * RS + h) * NA + k) * 32 + lane];
-      }
-    }
-    if (wc > 0) my = 0;  // only the first column warp of a slot finishes its rows
-  }
-#pragma unroll
-  for (int i = 0; i < RP; ++i) {
-    if (i < my) {
-#pragma unroll
-      for (int h = 0; h < RS; ++h)
-#pragma unroll
-        for (int k = 0; k < NA; ++k) {
-          T v = acc[i][h][k];
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-          acc[i][h][k] = v;
-        }
-    }
-  }
-
+  __syncthreads();
   LMS_TRACE_POINT(a, trace_base + 3);
-  // ---- epilogue: lane i*RS+h finishes row (i, h) ----
-#pragma unroll
-  for (int i = 0; i < RP; ++i) {
-#pragma unroll
-    for (int h = 0; h < RS; ++h) {
-      const long long row = (long long)(gw + i * GW) * RS + h;
-      if (lane == i * RS + h && i < my && row < a.n) {
-        const T* ri = rv[i][h];
-        const T* sum = acc[i][h];
-        if constexpr (MODE == kFwd) {
-          bool ok = true;
-          T qn[D];
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            const T hq = -a.inv_sig2 * sum[k];
-            const T hp = sum[D + k];
-            // q_{t+1} = q_t + dt*hp ; p_{t+1} = p_t - dt*hq   (shooting.hpp:205-209)
-            qn[k] = Math<T>::add_rn(ri[k], Math<T>::mul_rn(a.dt, hp));
-            const T pn = Math<T>::add_rn(ri[D + k], -Math<T>::mul_rn(a.dt, hq));
-            ok = ok && Math<T>::finite(qn[k]) && Math<T>::finite(pn);
-            out[(long long)k * a.stride + row] = qn[k];
-            out[(long long)(D + k) * a.stride + row] = pn;
-            if (epi & kEpiFirstStep) {
-              a.hp0[(long long)k * a.stride + row] = hp;
-              hsum += (double)ri[D + k] * (double)hp;
-            }
-          }
-          if (!ok) atomicMin(a.diverged, ((unsigned long long)(unsigned)step_no << 32) | 0xffffffffull);
-          if (epi & kEpiLastStep) {
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-              const T tg = a.target[(long long)k * a.stride + row];
-              const double df = (double)qn[k] - (double)tg;  // shooting.hpp:324-325
-              msum += df * df;
-              // alpha_T = 2*lambda*(q(1) - target), beta_T = 0   (shooting.hpp:290-296)
-              a.adj0[(long long)k * a.stride + row] = Math<T>::mul_rn(a.two_lambda, qn[k] - tg);
-              a.adj0[(long long)(D + k) * a.stride + row] = T(0);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            const T da = a.inv_sig2 * sum[k];
-            const T dbeta = sum[D + k];
-            // alpha += dt*d_alpha ; beta += dt*d_beta   (shooting.hpp:302-306)
-            const T an = Math<T>::add_rn(ri[2 * D + k], Math<T>::mul_rn(a.dt, da));
-            const T bn = Math<T>::add_rn(ri[3 * D + k], Math<T>::mul_rn(a.dt, dbeta));
-            out[(long long)k * a.stride + row] = an;
-            out[(long long)(D + k) * a.stride + row] = bn;
-            if (epi & kEpiGradOut)  // grad = beta_0 + hp(q0,p0)   (shooting.hpp:311-313)
-              a.grad_out[row * D + k] = (double)Math<T>::add_rn(bn, __ldcg(a.hp0 + (long long)k * a.stride + row));
-          }
+
+  // ---- epilogue: thread t finishes component t % D of the CTA's row t / D ----
+  const int t = threadIdx.x;
+  if (t < pl.s_b * RS * D) {
+    const int rl = t / D, k = t - rl * D;
+    const int sl = rl / RS, h = rl - sl * RS;
+    const long long row = (long long)pl.slot0 * RS + rl;
+    if (row < a.n) {
+      // the slot's pieces in ascending column order
+      T s0 = T(0), s1 = T(0);
+      const T* theirs = part + pl.epi_first * NV + h * NA + k;
+#pragma unroll 1
+      for (int i = 0; i < pl.epi_count; ++i, theirs += NV) {
+        s0 += theirs[0];
+        s1 += theirs[D];
+      }
+      const T* ri = rowbuf + sl * NRMAX * RS + h;  // component c of this row: ri[c * RS]
+      if constexpr (MODE == kFwd) {
+        const T hq = -a.inv_sig2 * s0;
+        const T hp = s1;
+        // q_{t+1} = q_t + dt*hp ; p_{t+1} = p_t - dt*hq   (shooting.hpp:205-209)
+        const T pk = ri[(D + k) * RS];
+        const T qn = Math<T>::add_rn(ri[k * RS], Math<T>::mul_rn(a.dt, hp));
+        const T pn = Math<T>::add_rn(pk, -Math<T>::mul_rn(a.dt, hq));
+        out[(long long)k * a.stride + row] = qn;
+        out[(long long)(D + k) * a.stride + row] = pn;
+        if (!(Math<T>::finite(qn) && Math<T>::finite(pn)))
+          atomicMin(a.diverged, ((unsigned long long)(unsigned)step_no << 32) | 0xffffffffull);
+        if (epi & kEpiFirstStep) {
+          a.hp0[(long long)k * a.stride + row] = hp;
+          hsum += (double)pk * (double)hp;
         }
+        if (epi & kEpiLastStep) {
+          const T tg = a.target[(long long)k * a.stride + row];
+          const double df = (double)qn - (double)tg;  // shooting.hpp:324-325
+          msum += df * df;
+          // alpha_T = 2*lambda*(q(1) - target), beta_T = 0   (shooting.hpp:290-296)
+          a.adj0[(long long)k * a.stride + row] = Math<T>::mul_rn(a.two_lambda, qn - tg);
+          a.adj0[(long long)(D + k) * a.stride + row] = T(0);
+        }
+      } else {
+        const T da = a.inv_sig2 * s0;
+        const T dbeta = s1;
+        // alpha += dt*d_alpha ; beta += dt*d_beta   (shooting.hpp:302-306)
+        const T an = Math<T>::add_rn(ri[(2 * D + k) * RS], Math<T>::mul_rn(a.dt, da));
+        const T bn = Math<T>::add_rn(ri[(3 * D + k) * RS], Math<T>::mul_rn(a.dt, dbeta));
+        out[(long long)k * a.stride + row] = an;
+        out[(long long)(D + k) * a.stride + row] = bn;
+        if (epi & kEpiGradOut)  // grad = beta_0 + hp(q0,p0)   (shooting.hpp:311-313)
+          a.grad_out[row * D + k] = (double)Math<T>::add_rn(bn, __ldcg(a.hp0 + (long long)k * a.stride + row));
       }
     }
   }
 }
 
-template <typename T, int D, int RP, int W>
-__global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T> a)
+template <typename T, int D>
+__global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const SmallArgs<T> a)
 {
-  constexpr int kThreadsHere = 32 * W;
+  constexpr int kThreadsHere = 32 * kSmallWarps;
   constexpr int RS = SmallShape<T>::kRowsPerSlot;
+  constexpr int NV = RS * 2 * D;
   extern __shared__ __align__(128) unsigned char small_smem[];
   T* tile = reinterpret_cast<T*>(small_smem);
-  __shared__ __align__(16) T part[(W - 1) * RP * RS * Shape<kFwd, D>::kAcc * 32];  // column-warp partial sums
+  __shared__ __align__(16) T part[kSmallWarps * 2 * NV];               // the pieces' sums
+  __shared__ __align__(16) T rowbuf[kSmallMaxSlots * RS * 4 * D];      // row operands for the epilogue threads
   __shared__ __align__(8) unsigned long long bars[SmallShape<T>::kMaxChunks];
   __shared__ double exp_tbl_all[sizeof(T) == 8 ? kExpTableDoubles : 1];  // fp64 only
   if (threadIdx.x == 0) {
@@ -427,29 +531,29 @@ __global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T
   small_grid_barrier(a.barrier, bar_target);
   if (bad_input) atomicMin(a.diverged, 0xffffffffull);  // step 0
 
+  const SmallPlan pl = small_plan<RS, D>(a.n);
   unsigned phase = 0;  // parity the chunk barriers complete next
   double hsum = 0.0, msum = 0.0;
   const int Tn = a.timesteps;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int GW = gridDim.x * a.wr;
+  const int GW = gridDim.x * kSmallWarps;
   // forward Euler flow, T+1 snapshots kept for the adjoint (shooting.hpp:199-212)
   for (int t = 0; t < Tn; ++t) {
     const unsigned epi = kEpiEuler | (t == 0 ? kEpiFirstStep : 0u) | (t == Tn - 1 ? kEpiLastStep : 0u);
-    small_step<T, D, kFwd, RP>(a, a.traj + (long long)t * a.snap_elems, nullptr,
-                               a.traj + (long long)(t + 1) * a.snap_elems, epi, t + 1, tile, part, bars, phase, hsum,
-                               msum, exp_tbl, 8 * t);
+    small_step<T, D, kFwd>(a, pl, a.traj + (long long)t * a.snap_elems, nullptr, a.traj + (long long)(t + 1) * a.snap_elems,
+                           epi, t + 1, tile, part, rowbuf, bars, phase, hsum, msum, exp_tbl, 8 * t);
     LMS_TRACE_POINT(a, 8 * t + 4);
     if (t == Tn - 1) {
-      // per-row-warp partials of the two double sums: lanes hold their rows' terms; fixed butterfly
+      // per-warp partials of the two double sums: threads hold their rows' terms; fixed butterfly
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) {
         hsum += __shfl_xor_sync(0xffffffffu, hsum, off);
         msum += __shfl_xor_sync(0xffffffffu, msum, off);
       }
-      if (lane == 0 && warp < a.wr) {
-        a.warp_part[blockIdx.x * a.wr + warp] = hsum;
-        a.warp_part[GW + blockIdx.x * a.wr + warp] = msum;
+      if (lane == 0) {
+        a.warp_part[blockIdx.x * kSmallWarps + warp] = hsum;
+        a.warp_part[GW + blockIdx.x * kSmallWarps + warp] = msum;
       }
     }
     small_grid_barrier(a.barrier, bar_target);
@@ -473,15 +577,19 @@ __global__ void __launch_bounds__(32 * W, 1) small_eval_kernel(const SmallArgs<T
       a.scalars[1] = h;
       a.scalars[2] = m;
       a.scalars[0] = h + a.lambda * m;
+      // host-buffer calls: the scalars live in mapped host memory; the divergence word (final after the last forward
+      // barrier: only the input check and the forward epilogues record) goes along as its fourth word
+      unsigned long long* word_out = reinterpret_cast<unsigned long long*>(a.scalars + 3);
+      if (word_out != a.diverged) *word_out = __ldcg(a.diverged);
     }
   }
   // discrete adjoint sweep t = T-1 .. 0 (shooting.hpp:300-307), final gradient fused into the t = 0 step
   T* adj_in = a.adj0;
   T* adj_out = a.adj1;
   for (int t = Tn - 1; t >= 0; --t) {
-    small_step<T, D, kAdj, RP>(a, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
-                               kEpiEuler | (t == 0 ? kEpiGradOut : 0u), t, tile, part, bars, phase, hsum, msum, exp_tbl,
-                               8 * (2 * Tn - 1 - t));
+    small_step<T, D, kAdj>(a, pl, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
+                           kEpiEuler | (t == 0 ? kEpiGradOut : 0u), t, tile, part, rowbuf, bars, phase, hsum, msum,
+                           exp_tbl, 8 * (2 * Tn - 1 - t));
     LMS_TRACE_POINT(a, 8 * (2 * Tn - 1 - t) + 4);
     T* tmp = adj_in;
     adj_in = adj_out;

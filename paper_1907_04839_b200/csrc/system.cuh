@@ -223,7 +223,7 @@ class System final : public SystemBase {
   void pick_kernels(bool partitioned);
   void alloc_exchange_arena();
   void plan_small();
-  void launch_small();
+  void launch_small(bool host_io = false);
   void p2p_exchange();
   void p2p_disconnect();
 
@@ -290,13 +290,15 @@ class System final : public SystemBase {
   bool small_enabled_ = true;     // LMS_SMALL=0 pins the tiled path
   int small_max_n_ = 0;           // largest n the persistent kernel is chosen for (LMS_SMALL_MAX_N)
   bool use_small_ = false;        // decided at bind
-  int small_grid_ = 0, small_threads_ = 0, small_wr_ = 0, small_wc_ = 1;
+  int small_grid_ = 0, small_threads_ = 0;
   int small_cluster_ = 1, small_grid_cap_ = 0;  // thread-block cluster size sharing the state fetch (TMA multicast)
   unsigned small_bar_count_ = 0;  // arrivals the barrier counter has seen so far (host-side mirror)
   size_t small_smem_ = 0;
   void (*small_fn_)(SmallArgs<T>) = nullptr;
   double* warp_part_ = nullptr;   // 2 x (SMs x kSmallMaxWarps) per-row-warp scalar partials
   unsigned* small_bar_ = nullptr; // grid barrier: monotonic arrival counter
+  double* h_zc_ = nullptr;        // mapped pinned x | grad | {loss, kinetic, mismatch, divergence word}: the persistent kernel reads and
+                                  // writes the host-buffer call's operands in place (no staging copies, no copy launches)
 
   // row partition (multi-GPU)
   int rank_ = 0, world_ = 1;

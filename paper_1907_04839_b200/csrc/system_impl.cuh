@@ -176,6 +176,7 @@ System<T, D>::~System()
   dev_free(d_x_);
   dev_free(d_ids_);
   if (h_scalars_) cudaFreeHost(h_scalars_);
+  if (h_zc_) cudaFreeHost(h_zc_);
   for (auto e : events_) cudaEventDestroy(e);
   if (ev_begin_) cudaEventDestroy(ev_begin_);
   if (ev_end_) cudaEventDestroy(ev_end_);
@@ -392,20 +393,17 @@ void System<T, D>::plan_small()
   if (stride_ % CH != 0 || ceil_div(n(), CH) > SmallShape<T>::kMaxChunks) return;  // every chunk gets its own buffer
   const int slots = ceil_div(n(), RS);
   const int grid = std::min(num_sms_, slots);
-  const int per_cta = ceil_div(slots, grid);  // slots of the busiest CTA
-  // One slot per row warp, sixteen warps; the spare warps split the columns of a slot (wc warps each).  (Several
-  // slots per warp on eight warps -- fewer shared-memory loads per pair, half the warps -- measured slower at every
-  // size the staged state fits: N = 2000 fp32 0.226 vs 0.206 ms, N = 3000 0.476 vs 0.380 ms.)
-  if (per_cta > kSmallMaxWarps) return;
-  const int rp = 1;
-  small_fn_ = small_eval_kernel<T, D, 1, 16>;
-  small_threads_ = 32 * 16;
-  small_wr_ = per_cta;
-  small_wc_ = kSmallMaxWarps / per_cta;
+  // A CTA's slots x 32-column groups are dealt to its sixteen warps in equal contiguous runs (small_kernels.cuh),
+  // so any slot count up to kSmallMaxSlots keeps every warp busy.  (Before: one slot per row warp, the spare warps
+  // splitting the columns evenly -- N = 3000 left 5 of 16 warps idle.)
+  if (ceil_div(slots, grid) > kSmallMaxSlots) return;
+  small_fn_ = small_eval_kernel<T, D>;
+  small_threads_ = 32 * kSmallWarps;
   int coop = 0;
   LMS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cfg.device));
   if (!coop) return;
-  small_smem_ = (size_t)ceil_div(n(), CH) * (4 * D) * CH * sizeof(T);
+  // one contiguous array of kCols columns per component; the last one only as long as the staged chunks
+  small_smem_ = ((size_t)(4 * D - 1) * SmallShape<T>::kCols + (size_t)ceil_div(n(), CH) * CH) * sizeof(T);
   LMS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(small_fn_), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)small_smem_));
   int per_sm = 0;
@@ -444,20 +442,14 @@ void System<T, D>::plan_small()
       break;
     }
   }
+  if (!h_zc_) LMS_CUDA(cudaHostAlloc(&h_zc_, (2 * (size_t)cfg.n * D + 4) * sizeof(double), cudaHostAllocMapped));
   if (small_cluster_ > 1) {
-    // re-plan the rows for the cluster-aligned grid
+    // cluster launches are whole clusters (CTAs without rows still fetch their share and take part in the barriers)
     const int g = std::min(small_grid_cap_, (int)round_up(grid, small_cluster_));
-    const int pc = ceil_div(slots, g);
-    if (rp == 1 && pc <= kSmallMaxWarps) {
-      small_wr_ = pc;
-      small_wc_ = kSmallMaxWarps / pc;
-      small_grid_ = g;
-    } else if (rp > 1 && ceil_div(pc, rp) <= 8) {
-      small_wr_ = ceil_div(pc, rp);
-      small_wc_ = 8 / small_wr_;
+    if (ceil_div(slots, g) <= kSmallMaxSlots) {
       small_grid_ = g;
     } else {
-      small_cluster_ = 1;  // the smaller grid would need another kernel shape: stay unclustered
+      small_cluster_ = 1;
       small_grid_ = grid;
     }
   } else {
@@ -467,10 +459,11 @@ void System<T, D>::plan_small()
 }
 
 template <typename T, int D>
-void System<T, D>::launch_small()
+void System<T, D>::launch_small(bool host_io)
 {
   SmallArgs<T> a{};
-  a.x = d_x_;
+  const size_t nd = (size_t)n() * D;
+  a.x = host_io ? h_zc_ : d_x_;
   a.traj = traj_;
   a.stride = stride_;
   a.snap_elems = (long long)kState * stride_;
@@ -478,15 +471,13 @@ void System<T, D>::launch_small()
   a.adj1 = adj_[1];
   a.hp0 = hp0_;
   a.target = target_;
-  a.grad_out = d_grad_;
+  a.grad_out = host_io ? h_zc_ + nd : d_grad_;
   a.warp_part = warp_part_;
-  a.scalars = d_scalars_;
+  a.scalars = host_io ? h_zc_ + 2 * nd : d_scalars_;
   a.diverged = d_diverged_;
   a.barrier = small_bar_;
   a.bar_base = small_bar_count_;
   small_bar_count_ += (unsigned)small_grid_ * (unsigned)(2 * timesteps);  // 1 + T + (T-1) barriers per launch
-  a.wr = small_wr_;
-  a.wc = small_wc_;
 #ifdef LMS_SMALL_TRACE
   a.trace = reinterpret_cast<unsigned long long*>(d_io_);  // staging scratch: idle during an evaluation
 #else
@@ -965,23 +956,46 @@ void System<T, D>::eval(const double* x, double* grad, double* scalars, bool dev
     LMS_CUDA(cudaGetLastError());
     traj0_is_q0_ = true;
   }
-  LMS_CUDA(cudaMemcpyAsync(d_x_, x, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                           stream_));
-  LMS_CUDA(cudaEventRecord(ev_begin_, stream_));
   const bool timed = kernel_timing;
-  if (use_small_ && !timed) {
-    launch_small();
-  } else if (graph_ && !timed) {
-    LMS_CUDA(cudaGraphLaunch(graph_, stream_));
-    last_eval_launches = graph_launches_;
+  // Small problems called with host buffers: the persistent kernel reads x from, and writes the gradient, the
+  // scalars and the divergence word to, mapped pinned memory -- no staging copies around the one launch.
+  const bool zero_copy = use_small_ && !timed && !device_ptrs && h_zc_ != nullptr;
+  if (zero_copy) {
+    const size_t nd = (size_t)n() * D;
+    std::memcpy(h_zc_, x, bytes);
+    LMS_CUDA(cudaEventRecord(ev_begin_, stream_));
+    launch_small(/*host_io=*/true);
+    LMS_CUDA(cudaEventRecord(ev_end_, stream_));
+    stored_t_ = timesteps;
+    sync();
+    std::memcpy(grad, h_zc_ + nd, bytes);
+    std::memcpy(h_scalars_, h_zc_ + 2 * nd, 4 * sizeof(double));
+    unsigned long long word;
+    std::memcpy(&word, h_scalars_ + 3, sizeof(word));
+    if (word != kNotDiverged) {
+      last_diverged_step = (int)(word >> 32);
+      const unsigned low = (unsigned)(word & 0xffffffffull);
+      last_diverged_point = low == 0xffffffffu ? -1 : (long long)low;
+      throw StatusError{LMS_ERR_DIVERGED, "non-finite state during integration"};
+    }
   } else {
-    enqueue_eval(timed);
+    LMS_CUDA(cudaMemcpyAsync(d_x_, x, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             stream_));
+    LMS_CUDA(cudaEventRecord(ev_begin_, stream_));
+    if (use_small_ && !timed) {
+      launch_small();
+    } else if (graph_ && !timed) {
+      LMS_CUDA(cudaGraphLaunch(graph_, stream_));
+      last_eval_launches = graph_launches_;
+    } else {
+      enqueue_eval(timed);
+    }
+    LMS_CUDA(cudaEventRecord(ev_end_, stream_));
+    LMS_CUDA(cudaMemcpyAsync(grad, d_grad_, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                             stream_));
+    stored_t_ = timesteps;
+    read_diverged_or_throw();  // synchronises
   }
-  LMS_CUDA(cudaEventRecord(ev_end_, stream_));
-  LMS_CUDA(cudaMemcpyAsync(grad, d_grad_, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                           stream_));
-  stored_t_ = timesteps;
-  read_diverged_or_throw();  // synchronises
   float ms = 0.f;
   LMS_CUDA(cudaEventElapsedTime(&ms, ev_begin_, ev_end_));
   last_eval_ms = ms;

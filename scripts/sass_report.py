@@ -15,7 +15,7 @@ KERNELS = [
     ("fp32 adjoint, N < 16 000 (`adj_f32x2_r2_j2_b5_u2`)", "pair_kernel<float, 3, 1, 2, 2, 5, true, 2, false, false, false>", "39 + 1 ex2"),
     ("fp64 forward (`fwd_f64_r2_j2_u2_tma`)", "pair_kernel<double, 3, 0, 2, 2, 3, false, 2, true, false, false>", "28"),
     ("fp64 adjoint (`adj_f64_r2_j2_u2_tma`)", "pair_kernel<double, 3, 1, 2, 2, 2, false, 2, true, false, false>", "50"),
-    ("persistent small-N kernel, fp32 (`small_eval_kernel<float,3>`)", "small_eval_kernel<float, 3,", "17 + 1 / 39 + 1"),
+    ("persistent small-N kernel, fp32 (`small_eval_kernel<float,3>`)", "small_eval_kernel<float, 3>", "17 + 1 / 39 + 1"),
 ]
 sass = subprocess.run(["cuobjdump", "-sass", SO], capture_output=True, text=True, check=True).stdout
 blocks = sass.split("Function : ")[1:]

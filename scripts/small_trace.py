@@ -23,9 +23,9 @@ for n in [int(v) for v in sys.argv[1:]] or [500, 1000, 2000]:
         s.lib.lms_debug_read_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
         s.lib.lms_debug_read_trace(s.handle, tr.ctypes.data, tr.size)
         tr = tr.reshape(2 * T, 8).astype(np.int64)
-        # columns: 0 step start, 1 first chunk landed, 2 sweep done, 3 sums combined, 4 epilogue done, 5 barrier passed
+        # columns: 0 step start, 1 row operands staged, 2 sweep + lane tree done (warp 0), 3 all warps done, 4 epilogue done, 5 barrier passed
         d = np.diff(tr[:, :6], axis=1)
-        names = ["first chunk", "sweep", "combine+butterfly", "epilogue", "barrier"]
+        names = ["rows staged", "sweep", "wait for warps", "epilogue", "barrier"]
         print(f"n={n} {prec}: device {s.last_eval_device_ms()*1e3:.1f} us; kernel span {(tr[-1,4]-tr[0,0])/1e3:.1f} us")
         for half, rows in (("forward", d[:T]), ("adjoint", d[T:])):
             print(f"   {half:8s} " + "  ".join(f"{nm} {np.median(rows[:, k])/1e3:.2f}" for k, nm in enumerate(names)) +

@@ -118,11 +118,13 @@ def test_compute_gradient_parity(hs, oracle, prec, n, T, lam, tiled_only):
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
 @pytest.mark.parametrize("dim", [2, 3])
-@pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 255, 256, 257, 511, 512, 513, 1184, 1185, 2369, 2900])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 31, 32, 33, 255, 256, 257, 295, 296, 297, 511, 512, 513, 1000, 1184, 1185, 2047, 2048,
+                               2049, 2369, 2900, 4095, 4096, 4097])
 def test_persistent_kernel_edge_sizes(hs, oracle, prec, dim, n):
-    """The persistent path at the sizes where its decomposition changes: fewer rows than one warp's slot, one
-    chunk of staged columns +- 1 (512 fp32 / 256 fp64), one and two slots per warp (148 SMs x 8 warps = 1184 warps),
-    an odd last row of a packed pair; odd T and even T end in different adjoint buffers.  Checked against the
+    """The persistent path at the sizes where its decomposition changes: fewer rows than one slot, fewer work items
+    than warps, one chunk of staged columns +- 1 (512 fp32 / 256 fp64), one slot per CTA +- 1 (148 SMs x 2 rows),
+    several slots per CTA (a warp's run then spans two slots), the shared-memory capacity +- 1 (4096 fp32 / 2048
+    fp64), an odd last row of a packed pair; odd T and even T end in different adjoint buffers.  Checked against the
     oracle, against the tiled path (same epilogue arithmetic, different summation order) and for run-to-run bits."""
     tol = TOL[prec]
     # constant landmark density (a denser cloud than ~500 per 14^dim box makes the flow itself ill-conditioned in fp32)
