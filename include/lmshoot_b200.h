@@ -119,6 +119,12 @@ int lms_objective_eval_device(lms_system* sys, const double* d_x, double* d_grad
  * registration.cpp:85-93). */
 int lms_objective_final_q(lms_system* sys, double* out);
 
+/* Registration metrics on the device (registration.cpp:39-40,95-96 -> landmarks.cpp:164-179 average_dist, max_dist):
+ * out[4] = {avg_before, max_before, avg_after, max_after}: template vs target as bound, and the warped landmarks
+ * q(1) of the last evaluation (widened to double as registration.cpp:88-92 does) vs target.  Per-point distances in
+ * double, the average as the reference's sequential sum: bit-identical to the reference's loops. */
+int lms_registration_metrics(lms_system* sys, double* out);
+
 /* Device time (ms, CUDA events on the library stream) of the compute part of the last evaluation
  * and the number of kernels it launched. */
 double lms_last_eval_device_ms(const lms_system* sys);

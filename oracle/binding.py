@@ -67,6 +67,7 @@ class CpuShooting:
             "integrate_forward": ([c_int, c_int, c_size_t, c_double, c_int, _dp, _dp, _dp, _dp] + red, c_int),
             "adjoint_step": ([c_int, c_int, c_size_t, c_double, _dp, _dp, _dp, _dp, _dp, _dp] + red, c_int),
             "mismatch_sq": ([c_int, c_int, c_size_t, _dp, _dp, _dp], c_int),
+            "landmark_distances": ([c_int, c_size_t, _dp, _dp, _dp], c_int),
             "compute_gradient": (
                 [c_int, c_int, c_size_t, c_double, c_double, c_int, _dp, _dp, _dp, _dp, _dp] + red,
                 c_int,
@@ -78,6 +79,8 @@ class CpuShooting:
             ),
         }
         for name, (argtypes, restype) in sig.items():
+            if name == "landmark_distances" and prefix == "ref":
+                continue  # landmarks.cpp needs Eigen (unbuildable here): restated in the C oracle only
             fn = getattr(lib, f"{prefix}_{name}")
             fn.argtypes = argtypes
             fn.restype = restype
@@ -170,6 +173,14 @@ class CpuShooting:
         out = c_double()
         self._check(self._mismatch_sq(PREC[prec], d, n, _p(a), _p(b), ctypes.byref(out)))
         return out.value
+
+    def landmark_distances(self, a, b):
+        """(average_dist, max_dist) of two paired landmark sets (landmarks.cpp:164-179)."""
+        a, b = _arr(a), _arr(b)
+        n, d = a.shape
+        out = np.zeros(2)
+        self._check(self._landmark_distances(d, n, _p(a), _p(b), _p(out)))
+        return float(out[0]), float(out[1])
 
     def compute_gradient(self, prec, q0, p0, target, sigma, lam, timesteps, strategy="blocked_tree", block=256,
                          threads=0):

@@ -302,6 +302,28 @@ int orc_mismatch_sq(int prec, int dim, size_t n, const double* a, const double* 
   return 0;
 }
 
+/* landmarks.cpp:148-161 pointwise_dist (double sum of squared coordinate differences, sqrt), :164-171 average_dist
+ * (sequential sum over the points / n), :173-179 max_dist (running std::max from 0).  n == 0: the reference divides
+ * 0 by 0; callers never pass empty sets (require_paired + registration.cpp:148-150), so {0, 0} is returned. */
+int orc_landmark_distances(int dim, size_t n, const double* a, const double* b, double* out)
+{
+  if (dim != 2 && dim != 3) return 1;
+  double sum = 0, best = 0;
+  for (size_t i = 0; i < n; ++i) {
+    double s = 0;
+    for (int c = 0; c < dim; ++c) {
+      double d = a[i * dim + c] - b[i * dim + c];
+      s += d * d;
+    }
+    double dist = sqrt(s);
+    sum += dist;
+    best = best > dist ? best : dist;
+  }
+  out[0] = n ? sum / (double)n : 0.0;
+  out[1] = best;
+  return 0;
+}
+
 int orc_compute_gradient(int prec, int dim, size_t n, double sigma, double lambda, int timesteps,
                          const double* q0, const double* p0, const double* target, double* scalars,
                          double* grad, int strategy, size_t block, unsigned threads)

@@ -39,6 +39,8 @@ int orc_adjoint_step(int prec, int dim, size_t n, double sigma, const double* q,
                      const double* alpha, const double* beta, double* d_alpha, double* d_beta,
                      int strategy, size_t block, unsigned threads);
 int orc_mismatch_sq(int prec, int dim, size_t n, const double* a, const double* b, double* out);
+/* average_dist / max_dist between paired double landmark sets (landmarks.cpp:148-179): out = {avg, max}. */
+int orc_landmark_distances(int dim, size_t n, const double* a, const double* b, double* out);
 int orc_compute_gradient(int prec, int dim, size_t n, double sigma, double lambda, int timesteps,
                          const double* q0, const double* p0, const double* target, double* scalars,
                          double* grad, int strategy, size_t block, unsigned threads);

@@ -78,6 +78,7 @@ SIGNATURES = {
     "lms_objective_eval": ([c_void_p, _dp, _dp, _dp, _dp, _dp], c_int),
     "lms_objective_eval_device": ([c_void_p, c_void_p, c_void_p, _dp], c_int),
     "lms_objective_final_q": ([c_void_p, _dp], c_int),
+    "lms_registration_metrics": ([c_void_p, _dp], c_int),
     "lms_last_eval_device_ms": ([c_void_p], c_double),
     "lms_last_eval_kernel_launches": ([c_void_p], c_int),
     "lms_set_kernel_timing": ([c_void_p, c_int], c_int),

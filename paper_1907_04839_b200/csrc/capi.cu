@@ -248,6 +248,11 @@ int lms_objective_final_q(lms_system* sys, double* out)
   return guarded(sys, [&](lms::SystemBase* s) { s->final_q(out); });
 }
 
+int lms_registration_metrics(lms_system* sys, double* out)
+{
+  return guarded(sys, [&](lms::SystemBase* s) { s->registration_metrics(out); });
+}
+
 double lms_last_eval_device_ms(const lms_system* sys) { return sys && sys->impl ? sys->impl->last_eval_ms : 0.0; }
 int lms_last_eval_kernel_launches(const lms_system* sys)
 {

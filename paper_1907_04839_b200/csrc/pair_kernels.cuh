@@ -135,7 +135,7 @@ struct Math<float> {
 //   4: 16 entries (128 B: every bank once, conflict-free for any index pattern), degree 6, |rel err| < 7.9e-18
 //   5: 32 entries, degree 5, < 1.5e-16        6: 64 entries, degree 4, < 2.5e-15
 // A larger table trades DP-pipe work (one DFMA per step) for shared-memory bank conflicts on the table load.
-// Measured on B200 (N = 20 000, T = 10 gradient; scripts/gpu_exp_ab.sh): 22.33 / 21.90 / 21.64 ms for B = 4 / 5 / 6
+// Measured on B200 (N = 20 000, T = 10 gradient; side-by-side builds with LMS_NVCC_EXTRA=-DLMS_EXP_BITS=..): 22.33 / 21.90 / 21.64 ms for B = 4 / 5 / 6
 // (degree 7 with 16 entries, the first version: 22.85 ms).  Default 5: the last setting below half an ulp.
 #ifndef LMS_EXP_BITS
 #define LMS_EXP_BITS 5
@@ -1071,6 +1071,35 @@ __global__ void mismatch_sequential(const T* __restrict__ a, const T* __restrict
       s = __dadd_rn(s, __dmul_rn(d, d));
     }
   *out = s;
+}
+
+// Registration metrics (landmarks.cpp:148-179): per-point Euclidean distance between two row-major double sets, in
+// double with explicit _rn operations (no contraction), then average_dist's strictly sequential sum and max_dist's
+// running maximum by one thread -- bit-identical to the reference's loops.
+template <int kUnused = 0>
+__global__ void point_distances(const double* __restrict__ a, const double* __restrict__ b, int n, int ncomp,
+                                double* __restrict__ dist)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int c = 0; c < ncomp; ++c) {
+    const double d = __dadd_rn(a[(long long)i * ncomp + c], -b[(long long)i * ncomp + c]);
+    s = __dadd_rn(s, __dmul_rn(d, d));
+  }
+  dist[i] = __dsqrt_rn(s);
+}
+template <int kUnused = 0>
+__global__ void avg_max_sequential(const double* __restrict__ dist, int n, double* __restrict__ out)
+{
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double sum = 0.0, best = 0.0;
+  for (int i = 0; i < n; ++i) {
+    sum = __dadd_rn(sum, dist[i]);
+    best = best > dist[i] ? best : dist[i];
+  }
+  out[0] = n > 0 ? __ddiv_rn(sum, (double)n) : 0.0;
+  out[1] = best;
 }
 
 }  // namespace lms

@@ -84,6 +84,7 @@ class SystemBase {
   virtual void bind(const double* q0, const double* target, double lambda, int timesteps) = 0;
   virtual void eval(const double* x, double* grad, double* scalars, bool device_ptrs) = 0;
   virtual void final_q(double* out) = 0;
+  virtual void registration_metrics(double* out) = 0;  // {avg, max} template-target, {avg, max} q(1)-target
   virtual void velocities(const double* q, const double* p, size_t m, const double* pts, double* out) = 0;
   virtual void warp_stored(size_t m, const double* pts, double* out) = 0;
   virtual void comm_init(const unsigned char* id, int rank, int world) = 0;
@@ -179,6 +180,7 @@ class System final : public SystemBase {
   void bind(const double* q0, const double* target, double lambda, int timesteps) override;
   void eval(const double* x, double* grad, double* scalars, bool device_ptrs) override;
   void final_q(double* out) override;
+  void registration_metrics(double* out) override;
   void velocities(const double* q, const double* p, size_t m, const double* pts, double* out) override;
   void warp_stored(size_t m, const double* pts, double* out) override;
   void comm_init(const unsigned char* id, int rank, int world) override;
@@ -271,6 +273,7 @@ class System final : public SystemBase {
   double* d_x_ = nullptr;
   double* d_grad_ = nullptr;
   double* h_scalars_ = nullptr;  // pinned: 3 doubles + the divergence word
+  double* d_metrics_ = nullptr;  // registration_metrics: {avg, max} before and after
   size_t io_cap_ = 0;
 
   // bound problem

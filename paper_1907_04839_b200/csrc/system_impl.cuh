@@ -84,6 +84,7 @@ System<T, D>::System(const lms_config& c, int batch_count)
   scratch_out_ = dev_alloc_zero<T>(kState * plane);
   d_scalars_ = dev_alloc_zero<double>(4 * B);
   d_diverged_ = reinterpret_cast<unsigned long long*>(d_scalars_ + 3);
+  d_metrics_ = dev_alloc_zero<double>(4);
   io_cap_ = (size_t)N * D * B;
   d_io_ = dev_alloc_zero<double>(4 * io_cap_);
   d_x_ = dev_alloc_zero<double>(std::max((size_t)stride_ * D, B * (size_t)N * D));
@@ -172,6 +173,7 @@ System<T, D>::~System()
   dev_free(warp_part_);
   dev_free(small_bar_);
   dev_free(d_scalars_);
+  dev_free(d_metrics_);
   dev_free(d_io_);
   dev_free(d_x_);
   dev_free(d_ids_);
@@ -1022,6 +1024,38 @@ void System<T, D>::final_q(double* out)
   if (n() == 0) return;
   download(snapshot(stored_t_), stride_, out, n(), D);
   sync();
+}
+
+// average_dist / max_dist of (template, target) and of (warped = q(1) of the stored trajectory, target), on the
+// device (registration.cpp:39-40,95-96; landmarks.cpp:164-179).  The sets are the reference's double landmark sets:
+// the bound template / target as given, q(1) widened from the working precision (registration.cpp:88-92).
+template <typename T, int D>
+void System<T, D>::registration_metrics(double* out)
+{
+  require_single("registration metrics need a single-problem handle");
+  if (!bound) throw StatusError{LMS_ERR_STATE, "lms_bind_registration must precede the metrics"};
+  if (stored_t_ < 0) throw StatusError{LMS_ERR_STATE, "no stored trajectory"};
+  if (n() == 0) {
+    out[0] = out[1] = out[2] = out[3] = 0.0;
+    return;
+  }
+  const size_t nd = (size_t)n() * D;  // d_io_ holds 4 * io_cap_ >= 4 nd doubles: a | b | distances
+  double* a = d_io_;
+  double* b = d_io_ + nd;
+  double* dist = d_io_ + 2 * nd;         // n <= nd doubles
+  double* res = d_metrics_;
+  const int blocks = ceil_div(n(), 256);
+  LMS_CUDA(cudaMemcpyAsync(a, host_q0.data(), nd * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  LMS_CUDA(cudaMemcpyAsync(b, host_target.data(), nd * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  point_distances<><<<blocks, 256, 0, stream_>>>(a, b, n(), D, dist);
+  avg_max_sequential<><<<1, 32, 0, stream_>>>(dist, n(), res);
+  planes_to_aos<T><<<ceil_div((long long)nd, 256), 256, 0, stream_>>>(snapshot(stored_t_), stride_, a, n(), D);
+  point_distances<><<<blocks, 256, 0, stream_>>>(a, b, n(), D, dist);
+  avg_max_sequential<><<<1, 32, 0, stream_>>>(dist, n(), res + 2);
+  LMS_CUDA(cudaGetLastError());
+  LMS_CUDA(cudaMemcpyAsync(h_scalars_, res, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  for (int k = 0; k < 4; ++k) out[k] = h_scalars_[k];
 }
 
 // q(1) of every problem of the batch: batch x n x D.

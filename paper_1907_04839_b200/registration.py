@@ -33,7 +33,8 @@ class RegistrationResult:
 
 
 def average_dist(a, b):
-    """landmarks.cpp:164-171."""
+    """landmarks.cpp:164-171 on the host (numpy), for callers without a device handle; register_landmarks itself
+    takes the metrics from the device (lms_registration_metrics)."""
     return float(np.mean(np.linalg.norm(np.asarray(a) - np.asarray(b), axis=1))) if len(a) else 0.0
 
 
@@ -74,6 +75,10 @@ def register_landmarks(template, target, config: ShootingConfig | None = None, g
         _lib.check(entry(system.handle, ctypes.byref(params), momenta.ctypes.data_as(dp),
                                     warped.ctypes.data_as(dp), ctypes.byref(res), hist.ctypes.data_as(dp)),
                    system.handle)
+        # avg / max landmark distance before and after (registration.cpp:39-40,95-96), computed on the device from
+        # the bound sets and the resident q(1)
+        metrics = np.zeros(4)
+        _lib.check(lib.lms_registration_metrics(system.handle, metrics.ctypes.data_as(dp)), system.handle)
     finally:
         if own:
             system.close()
@@ -81,6 +86,6 @@ def register_landmarks(template, target, config: ShootingConfig | None = None, g
         momenta=momenta, warped=warped, final_loss=res.loss, initial_loss=res.initial_loss,
         evaluations=res.evaluations, iterations=res.iterations, reason=STOP_REASONS[res.reason],
         hist_loss=hist[: res.iterations].copy(),
-        avg_before=average_dist(template, target), max_before=max_dist(template, target),
-        avg_after=average_dist(warped, target), max_after=max_dist(warped, target),
+        avg_before=float(metrics[0]), max_before=float(metrics[1]),
+        avg_after=float(metrics[2]), max_after=float(metrics[3]),
     )

@@ -1,14 +1,14 @@
 #!/bin/bash
-# One GPU session: the -m gpu tests, the default bench line, the 1-GPU anchor of configs[2], and a two-rank
-# launcher / exchange check on the one GPU.  Everything lands in gpurun_out/.  Usage: gpurun -- bash scripts/gpu_session.sh [tag]
-tag=${1:-r2}
+# One GPU session: -m gpu tests, default bench, fp64 bench, reference arm, configs[0], small-N A/B, ncu (fp32 + fp64).
+tag=${1:-r2c}
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_pytest.log 2>&1; echo "pytest rc=$?" | tee -a gpurun_out/${tag}_pytest.log
-tail -5 gpurun_out/${tag}_pytest.log
-python bench.py --steps 10 --warmup 3 > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err; echo "bench rc=$?"
-cat gpurun_out/${tag}_bench.json | cut -c1-1500
-python bench.py --gpus 1 --landmarks 200000 --timesteps 20 --steps 3 --warmup 3 --no-extras > gpurun_out/${tag}_bench_c2_1gpu.json 2> gpurun_out/${tag}_bench_c2.err; echo "c2 rc=$?"
-cat gpurun_out/${tag}_bench_c2_1gpu.json | cut -c1-600
-python bench.py --gpus 2 --landmarks 20000 --timesteps 10 --steps 3 --warmup 3 > gpurun_out/${tag}_bench_2rank_oversub.json 2> gpurun_out/${tag}_bench_2rank.err; echo "2rank rc=$?"
-cat gpurun_out/${tag}_bench_2rank_oversub.json | cut -c1-1200
-tail -3 gpurun_out/${tag}_bench_2rank.err
+nvidia-smi --query-gpu=name,clocks.max.sm,clocks.sm,power.limit --format=csv > gpurun_out/${tag}_smi.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_pytest.log 2>&1; echo "pytest rc=$?" | tee -a gpurun_out/${tag}_pytest.log; tail -4 gpurun_out/${tag}_pytest.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err; echo "bench rc=$?"
+timeout 300 python bench.py --steps 10 --warmup 3 --precision f64 --no-extras > gpurun_out/${tag}_bench_f64.json 2>> gpurun_out/${tag}_bench.err
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${tag}_bench_reference.json 2>> gpurun_out/${tag}_bench.err; echo "ref rc=$?"
+timeout 300 python scripts/gpu_c1.py > gpurun_out/${tag}_c1.log 2>&1; cat gpurun_out/${tag}_c1.log
+timeout 600 python scripts/small_ab.py gpurun_out/${tag}_small_ab.json > gpurun_out/${tag}_small_ab.log 2>&1; tail -20 gpurun_out/${tag}_small_ab.log | cut -c1-400
+bash scripts/gpu_ncu.sh ${tag}_f32 > /dev/null 2>&1
+bash scripts/gpu_ncu.sh ${tag}_f64 --precision f64 > /dev/null 2>&1
+ls -la gpurun_out | tail -30

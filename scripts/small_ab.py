@@ -7,6 +7,7 @@ import sys
 import time
 
 import numpy as np
+import torch
 
 sys.path.insert(0, ".")
 from paper_1907_04839_b200 import HamiltonianSystem, make_template_points, rng_normals  # noqa: E402
@@ -27,14 +28,19 @@ for n in sizes:
         for name, tiled in (("persistent", False), ("tiled", True)):
             s = HamiltonianSystem(SIGMA, n, 3, prec, max_timesteps=T, tiled_only=tiled)
             s.bind_registration(q0, target, LAM, T)
+            # device ms: x / grad resident in HBM (CUDA events around the evaluation); wall ms: the host-buffer call
+            xd = torch.from_numpy(x0).cuda()
+            gd = torch.empty_like(xd)
             for _ in range(5):
                 s.objective(x0)
+                s.objective_ptrs(xd.data_ptr(), gd.data_ptr(), device=True)
             launches = s.last_eval_kernel_launches()
             ms, wall = [], []
             for _ in range(30):
                 t0 = time.perf_counter()
                 s.objective(x0)
                 wall.append((time.perf_counter() - t0) * 1e3)
+                s.objective_ptrs(xd.data_ptr(), gd.data_ptr(), device=True)
                 ms.append(s.last_eval_device_ms())
             s.close()
             dev = float(np.median(ms))

@@ -2,6 +2,7 @@
 T = 10.  usage: LMS_LIB_PATH=... python scripts/small_variants.py [prec] [sizes...]"""
 import sys
 import numpy as np
+import torch
 sys.path.insert(0, ".")
 from paper_1907_04839_b200 import HamiltonianSystem, make_template_points, rng_normals  # noqa: E402
 
@@ -15,11 +16,13 @@ for n in sizes:
     x0 = np.ascontiguousarray(((target - q0) / T).ravel())
     s = HamiltonianSystem(1.5, n, 3, prec, max_timesteps=T)
     s.bind_registration(q0, target, 5e5, T)
+    xd = torch.from_numpy(x0).cuda()
+    gd = torch.empty_like(xd)
     for _ in range(5):
-        s.objective(x0)
+        s.objective_ptrs(xd.data_ptr(), gd.data_ptr(), device=True)
     ms = []
     for _ in range(30):
-        s.objective(x0)
+        s.objective_ptrs(xd.data_ptr(), gd.data_ptr(), device=True)
         ms.append(s.last_eval_device_ms())
     out.append(f"{n}: {np.median(ms):.4f} ({s.last_eval_kernel_launches()})")
     s.close()

@@ -5,6 +5,7 @@ import sys
 import time
 
 import numpy as np
+import torch
 
 sys.path.insert(0, ".")
 from paper_1907_04839_b200 import HamiltonianSystem, make_template_points, rng_normals  # noqa: E402
@@ -26,6 +27,9 @@ for n in sizes:
         s = HamiltonianSystem(SIGMA, n, 3, prec, max_timesteps=T)
         s.bind_registration(q0, target, LAM, T)
         reps = 20 if n <= 20000 else (5 if n <= 100000 else (2 if n <= 200000 else 1))
+        # device ms: x / grad resident in HBM (CUDA events around the evaluation); wall ms: the host-buffer call
+        xd = torch.from_numpy(x0).cuda()
+        gd = torch.empty_like(xd)
         for _ in range(3 if n <= 100000 else 1):
             s.objective(x0)
         ms, wall = [], []
@@ -33,6 +37,8 @@ for n in sizes:
             t0 = time.perf_counter()
             s.objective(x0)
             wall.append((time.perf_counter() - t0) * 1e3)
+            if n <= 20000:
+                s.objective_ptrs(xd.data_ptr(), gd.data_ptr(), device=True)
             ms.append(s.last_eval_device_ms())
         s.close()
         dev = float(np.median(ms))

@@ -5,6 +5,8 @@ BASELINE.json's full sizes -- through row subsets and size-independent propertie
 Tolerances (BASELINE.json north_star / BASELINE.md §4): loss, H and ||dg||_inf/||g||_inf per evaluation
 within 1e-10 in fp64 and 1e-5 in fp32 (at well-conditioned evaluation points); integer/index results and
 the strictly sequential double sums are bit-exact."""
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -498,9 +500,36 @@ def test_hundred_iteration_registration_n1000(oracle, reference):
     assert np.abs(got.warped - want["warped"]).max() <= 1e-6
     assert got.final_loss == pytest.approx(want["loss"], rel=1e-6)
     assert got.avg_after < 1e-2 * got.avg_before
+    # the registration metrics come from the device (lms_registration_metrics): bit-identical to the reference's
+    # average_dist / max_dist loops (landmarks.cpp:164-179) on the same double sets
+    assert (got.avg_before, got.max_before) == oracle.landmark_distances(q0, target)
+    assert (got.avg_after, got.max_after) == oracle.landmark_distances(got.warped, target)
     cfg32 = ShootingConfig(sigma=SIGMA, timesteps=T, lam=lam, max_iter=100, precision="f32")
     got32 = register_landmarks(q0, target, cfg32)
     assert np.abs(got32.warped - want["warped"]).max() <= 5e-3
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("n,dim", [(1, 3), (257, 2), (5000, 3)])
+def test_registration_metrics_on_device(hs, oracle, prec, n, dim):
+    """avg / max landmark distance before and after (registration.cpp:39-40,95-96) from the device against the
+    restated landmarks.cpp:164-179 loops: bitwise, both for the bound double sets and for q(1) widened from the
+    working precision; and the state errors."""
+    from paper_1907_04839_b200 import HamiltonianSystem, _lib
+    from paper_1907_04839_b200.errors import StateError
+
+    q, p, target, *_ = synth_case(n, dim, 77 + n, spread=7.0 * max(1.0, (n / 500.0) ** (1.0 / dim)))
+    s = HamiltonianSystem(SIGMA, n, dim, prec, max_timesteps=4)
+    out = np.zeros(4)
+    dp = out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    with pytest.raises(StateError):
+        _lib.check(s.lib.lms_registration_metrics(s.handle, dp), s.handle)  # nothing bound
+    s.bind_registration(q, target, 25.0, 4)
+    s.objective(np.ascontiguousarray(p.ravel()))
+    _lib.check(s.lib.lms_registration_metrics(s.handle, dp), s.handle)
+    assert tuple(out[:2]) == oracle.landmark_distances(q, target)
+    assert tuple(out[2:]) == oracle.landmark_distances(s.final_q(), target)
+    s.close()
 
 
 def test_reference_minimize_drives_cuda_objective_through_cpp_adapter():

@@ -239,3 +239,20 @@ def test_pair_rows_equal_full_calls(oracle):
             da, db = oracle.adjoint_step(prec, q, p, alpha, beta, SIGMA)
             got = oracle.pair_rows(prec, q, p, rows, SIGMA, alpha, beta)
             assert np.array_equal(got[0], da[rows]) and np.array_equal(got[1], db[rows])
+
+
+def test_landmark_distances_restatement(oracle):
+    """average_dist / max_dist (landmarks.cpp:148-179): hand-checked values (3-4-5 and 5-12-13 triangles, a
+    coincident pair), the sequential-sum order, and two dimensions."""
+    a = np.array([[0.0, 0.0, 0.0], [1.0, 1.0, 1.0], [2.0, 0.0, -1.0]])
+    b = np.array([[3.0, 4.0, 0.0], [1.0, 1.0, 1.0], [2.0, 5.0, 11.0]])
+    avg, mx = oracle.landmark_distances(a, b)
+    assert avg == (5.0 + 0.0 + 13.0) / 3.0 and mx == 13.0
+    rng = np.random.default_rng(5)
+    a2, b2 = rng.normal(size=(1000, 2)), rng.normal(size=(1000, 2))
+    avg2, mx2 = oracle.landmark_distances(a2, b2)
+    dist = [float(np.sqrt((x[0] - y[0]) * (x[0] - y[0]) + (x[1] - y[1]) * (x[1] - y[1]))) for x, y in zip(a2, b2)]
+    total = 0.0
+    for d in dist:
+        total += d  # the reference's sequential order
+    assert avg2 == total / 1000.0 and mx2 == max(dist)
