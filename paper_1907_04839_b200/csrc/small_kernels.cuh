@@ -202,6 +202,12 @@ __device__ __forceinline__ void load_cols(const T* p, T (&v)[U])
 #ifndef LMS_SMALL_UA
 #define LMS_SMALL_UA 2
 #endif
+#ifndef LMS_SMALL_UF64
+#define LMS_SMALL_UF64 2
+#endif
+#ifndef LMS_SMALL_UA64
+#define LMS_SMALL_UA64 1
+#endif
 
 // What a thread needs to know about the CTA's work list; the same for every time step, so it is worked out once
 // per launch (the per-step code between two sweeps is latency-critical and mostly cold in the instruction cache:
@@ -218,7 +224,8 @@ template <int RS, int D>
 __device__ __forceinline__ SmallPlan small_plan(int n)
 {
   SmallPlan p;
-  const int warp = threadIdx.x >> 5;
+  // (the lane-0 shuffle tells ptxas the warp index -- and every count derived from it -- is warp-uniform)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int slots = (n + RS - 1) / RS;
   p.slot0 = (int)((long long)blockIdx.x * slots / gridDim.x);
   p.s_b = (int)((long long)(blockIdx.x + 1) * slots / gridDim.x) - p.slot0;
@@ -324,7 +331,7 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
   const unsigned bars_u32 = smem_u32(bars);
 
   // ---- the warp's pieces: (slot, groups [g0, g1)) ----
-  constexpr int U = F32 ? (MODE == kAdj ? LMS_SMALL_UA : LMS_SMALL_UF) : (MODE == kAdj ? 1 : 2);
+  constexpr int U = F32 ? (MODE == kAdj ? LMS_SMALL_UA : LMS_SMALL_UF) : (MODE == kAdj ? LMS_SMALL_UA64 : LMS_SMALL_UF64);
   int waited = 0;  // chunks [0, waited) have landed
 #pragma unroll 1
   for (int pc = 0; pc < pl.n_pieces; ++pc) {
@@ -373,8 +380,17 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
         pair_term<T, D, MODE>(rv[0], cj, acc, a.kexp, a.inv_sig2, exp_tbl);
       }
     };
-    auto need = [&](int g_last) {  // the chunks up to the one holding group g_last have landed
-      const int c = g_last / GPC;
+    // The piece chunk by chunk: a chunk is waited for once (they land roughly in order, so everything up to it is
+    // waited for), then its groups are swept without further checks -- blocks of U groups (lane l takes the U
+    // consecutive columns 32 U b + U l ..: one vector load per component), then single groups up to the chunk's
+    // end.  Chunks start at multiples of 16 groups, so only a piece's first chunk can have such a remainder.
+    // Counters and offsets are warp-uniform (uniform datapath: no vector-register reads in the loop control).
+    const T* lane_blk = tile + lane * U;
+    const T* lane_one = tile + lane;
+    int g = g0;
+#pragma unroll 1
+    while (g < g1) {
+      const int c = (int)((unsigned)g / (unsigned)GPC);
       if (c >= waited) {
 #pragma unroll 1
         do {
@@ -382,34 +398,30 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
           ++waited;
         } while (waited <= c);
       }
-    };
-
-    // blocks of U groups: lane l takes the U consecutive columns 32 U b + U l ...; then single groups
-    int g = g0;
-    const T* cp = tile + (long long)g * 32 + (long long)lane * U;
+      const int gend = (c + 1) * GPC < g1 ? (c + 1) * GPC : g1;
 #pragma unroll 1
-    for (; g + U <= g1; g += U, cp += 32 * U) {
-      need(g + U - 1);
-      T cj[U][NC];
+      for (; g + U <= gend; g += U) {
+        const T* cp = lane_blk + g * 32;
+        T cj[U][NC];
 #pragma unroll
-      for (int k = 0; k < NC; ++k) {
-        T v[U];
-        load_cols<T, U>(cp + k * NTOT, v);
+        for (int k = 0; k < NC; ++k) {
+          T v[U];
+          load_cols<T, U>(cp + k * NTOT, v);
 #pragma unroll
-        for (int u = 0; u < U; ++u) cj[u][k] = v[u];
+          for (int u = 0; u < U; ++u) cj[u][k] = v[u];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) evaluate(cj[u]);
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) evaluate(cj[u]);
-    }
-    if constexpr (U > 1) {
-      const T* cs = tile + (long long)g * 32 + lane;
+      if constexpr (U > 1) {
 #pragma unroll 1
-      for (; g < g1; ++g, cs += 32) {
-        need(g);
-        T cj[NC];
+        for (; g < gend; ++g) {
+          const T* cs = lane_one + g * 32;
+          T cj[NC];
 #pragma unroll
-        for (int k = 0; k < NC; ++k) cj[k] = cs[k * NTOT];
-        evaluate(cj);
+          for (int k = 0; k < NC; ++k) cj[k] = cs[k * NTOT];
+          evaluate(cj);
+        }
       }
     }
 
