@@ -638,6 +638,8 @@ def batch_arm(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
     dev_ms = wall_ms = 0.0
     for _ in range(K):
         flush.fill_(1)
@@ -646,6 +648,7 @@ def batch_arm(args):
         br.evaluate_ptrs(h_x.data_ptr(), h_grad.data_ptr(), h_scalars.data_ptr())  # pinned host buffers
         wall_ms += (time.perf_counter() - t0) * 1e3
         dev_ms += br.last_eval_device_ms()
+    clocks = sampler.result()
     if world > 1:
         t = torch.tensor([dev_ms, wall_ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -661,8 +664,22 @@ def batch_arm(args):
         "e2e": {"value": units * K / (wall_ms * 1e-3), "unit": "pair-evals/s", "h2d_bytes_per_step": int(x0.nbytes),
                 "d2h_bytes_per_step": int(x0.nbytes) + 32 * B, "ms_per_step": wall_ms / K},
         "gpu_launches": (2 * T + 2) * K,
+        "clocks": clocks,
         "registrations_per_sec_per_gradient": B * world * K / (dev_ms * 1e-3),
     }
+    # whole batched gradient against the CUDA-core pipe (the per-kernel split is the single-problem arm's business):
+    # contract slots per pair, forward + adjoint = 61 (fp64: 95), SURVEY.md section 8(d)
+    peaks, peaks_src = measured_peaks()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    lanes = 128 if args.precision == "f32" else 64
+    slots = (61.0 if args.precision == "f32" else 95.0) * T * float(n) * float(n) * B
+    peak = 148 * lanes * sm_mhz * 1e6 / 1e12
+    achieved = slots / (dev_ms / K * 1e-3) / 1e12
+    line["roofline"] = {"bound": "fp32_cuda_core" if args.precision == "f32" else "fp64_cuda_core",
+                        "kernel": "whole batched gradient (T forward + T adjoint pair-kernel launches over all problems)",
+                        "achieved": achieved, "peak": peak, "unit": "Tslot/s (FP lane-instructions)",
+                        "frac": achieved / peak, "traffic": None,
+                        "peak_source": f"148 SM x {lanes} lanes x sm_max_mhz {sm_mhz:.0f} MHz ({peaks_src} MEASURED_PEAKS.json)"}
     br.close()
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -78,6 +78,15 @@ class DeviceObjective {
   }
 
   void final_q(std::span<double> out) const { throw_status(lms_objective_final_q(sys_, out.data()), sys_); }
+  // {avg_before, max_before, avg_after, max_after}: average_dist / max_dist of (template, target) and of
+  // (q(1) of the last evaluation, target) -- registration.cpp:39-40,95-96 -- computed on the device
+  struct Metrics { double avg_before, max_before, avg_after, max_after; };
+  Metrics metrics() const
+  {
+    double m[4];
+    throw_status(lms_registration_metrics(sys_, m), sys_);
+    return {m[0], m[1], m[2], m[3]};
+  }
   double last_kinetic() const { return kinetic_; }
   double last_mismatch() const { return mismatch_; }
   long evaluations() const { return evaluations_; }
