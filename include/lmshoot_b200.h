@@ -213,7 +213,9 @@ int lms_batch_final_q(lms_system* sys, double* out);
  * minimize (lbfgs.hpp:81-82) on a host thread; concurrent objective calls are coalesced into one batched
  * device evaluation per round.  momenta_out / warped_out: batch x n x dim; results / status: batch entries
  * (status = LMS_OK, LMS_ERR_DIVERGED or LMS_ERR_NUMERICAL per problem).  At most LMS_BATCH_REGISTER_MAX problems
- * per call (LMS_ERR_INVALID beyond). */
+ * per call (LMS_ERR_INVALID beyond).  From 32 problems on the population is evaluated in two alternating groups, so
+ * that the host-side L-BFGS arithmetic of one group overlaps the device evaluation of the other (LMS_BATCH_GROUPS in
+ * the environment overrides the group count); *rounds_out counts the batched device evaluations of all groups. */
 #define LMS_BATCH_REGISTER_MAX 4096 /* problems per lms_batch_register call (one host thread each) */
 int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* momenta_out, double* warped_out,
                        lms_minimize_result* results, int* status, int* rounds_out);

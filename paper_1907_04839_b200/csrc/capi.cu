@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <condition_variable>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -394,23 +395,60 @@ int lms_register(lms_system* sys, const lms_lbfgs_params* params, double* moment
 namespace {
 
 // Every optimiser thread submits its trial point and sleeps; the last submitter of a round launches one batched
-// evaluation for all waiting problems and wakes them.  The drivers stay unchanged blocking callbacks.
+// evaluation for all waiting problems of its group and wakes them.  The drivers stay unchanged blocking callbacks.
+// The population is cut into groups with a rendezvous each: while the GPU evaluates one group's round, the host
+// threads of the other groups run their L-BFGS vector arithmetic (strictly sequential sums, the reference's order:
+// ~0.3 ms per iteration and problem at N = 2000), so the device does not idle between rounds.  Evaluations of one
+// handle are serialised by `eval_mutex`.
+struct PinnedDoubles {  // staging the device copies read / write directly (pageable vectors cost ~1 ms per 6 MB copy)
+  double* p = nullptr;
+  size_t n = 0;
+  bool pinned = false;
+  void assign(size_t count)
+  {
+    n = count;
+    if (cudaHostAlloc(&p, std::max<size_t>(count, 1) * sizeof(double), cudaHostAllocDefault) == cudaSuccess) {
+      pinned = true;
+    } else {
+      cudaGetLastError();
+      p = new double[std::max<size_t>(count, 1)];
+    }
+    std::memset(p, 0, std::max<size_t>(count, 1) * sizeof(double));
+  }
+  ~PinnedDoubles()
+  {
+    if (pinned) cudaFreeHost(p);
+    else delete[] p;
+  }
+  double* data() { return p; }
+};
+
 struct Rendezvous {
   lms_system* sys;
+  std::mutex* eval_mutex;  // one batched evaluation of the handle at a time
   size_t per;  // n * dim
+  int batch = 0;  // problems of the handle (all groups)
   std::mutex m;
   std::condition_variable cv;
   int active = 0, submitted = 0, rounds = 0;
   unsigned long long round = 0;
   std::vector<int> waiting;  // problem ids submitted this round
-  std::vector<double> x, grad, scalars;
-  std::vector<int> diverged;
+  PinnedDoubles *x, *grad;   // full-batch staging shared by the groups (disjoint problem ranges)
+  std::vector<double>* scalars;
+  std::vector<int>* diverged;
   int failure = LMS_OK;  // a CUDA-level failure aborts everybody
 
-  void run_round()  // caller holds the lock; everyone else is asleep
+  void run_round()  // caller holds the lock; everyone else of this group is asleep
   {
-    int rc = lms_batch_eval(sys, waiting.size(), waiting.data(), x.data(), grad.data(), scalars.data(),
-                            diverged.data());
+    // ascending ids: the device copies coalesce runs of neighbours; the whole population goes without an id list
+    std::sort(waiting.begin(), waiting.end());
+    const bool all = (int)waiting.size() == batch;
+    int rc;
+    {
+      std::lock_guard<std::mutex> device(*eval_mutex);
+      rc = lms_batch_eval(sys, all ? (size_t)batch : waiting.size(), all ? nullptr : waiting.data(), x->data(),
+                          grad->data(), scalars->data(), diverged->data());
+    }
     if (rc != LMS_OK) failure = rc;
     waiting.clear();
     submitted = 0;
@@ -431,7 +469,7 @@ double batched_objective(void* user, const double* x, double* grad, size_t n)
   ProblemCtx* ctx = static_cast<ProblemCtx*>(user);
   Rendezvous& rv = *ctx->rv;
   std::unique_lock<std::mutex> lock(rv.m);
-  std::memcpy(rv.x.data() + ctx->id * rv.per, x, n * sizeof(double));
+  std::memcpy(rv.x->data() + ctx->id * rv.per, x, n * sizeof(double));
   rv.waiting.push_back(ctx->id);
   ++rv.submitted;
   const unsigned long long my_round = rv.round;
@@ -440,12 +478,12 @@ double batched_objective(void* user, const double* x, double* grad, size_t n)
   else
     rv.cv.wait(lock, [&] { return rv.round != my_round || rv.failure != LMS_OK; });
   if (rv.failure != LMS_OK) throw rv.failure;
-  if (rv.diverged[ctx->id] >= 0) {
-    ctx->diverged_step = rv.diverged[ctx->id];
+  if ((*rv.diverged)[ctx->id] >= 0) {
+    ctx->diverged_step = (*rv.diverged)[ctx->id];
     throw (int)LMS_ERR_DIVERGED;  // aborts this problem's minimize, as DivergedError does in the reference
   }
-  std::memcpy(grad, rv.grad.data() + ctx->id * rv.per, n * sizeof(double));
-  return rv.scalars[3 * ctx->id];
+  std::memcpy(grad, rv.grad->data() + ctx->id * rv.per, n * sizeof(double));
+  return (*rv.scalars)[3 * ctx->id];
 }
 
 }  // namespace
@@ -464,21 +502,37 @@ int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* 
     return LMS_ERR_INVALID;
   }
   const size_t per = s->host_q0.size() / (size_t)B;
-  Rendezvous rv;
-  rv.sys = sys;
-  rv.per = per;
-  rv.active = B;
-  rv.x.assign(per * B, 0.0);
-  rv.grad.assign(per * B, 0.0);
-  rv.scalars.assign(3 * (size_t)B, 0.0);
-  rv.diverged.assign(B, -1);
+  // groups of problems with a rendezvous each (see Rendezvous); LMS_BATCH_GROUPS overrides
+  int groups = B >= 32 ? 2 : 1;
+  if (const char* e = std::getenv("LMS_BATCH_GROUPS")) groups = std::max(1, std::min(std::atoi(e), B));
+  std::mutex eval_mutex;
+  PinnedDoubles x_all, grad_all;
+  x_all.assign(per * B);
+  grad_all.assign(per * B);
+  std::vector<double> scalars_all(3 * (size_t)B, 0.0);
+  std::vector<int> diverged_all(B, -1);
+  std::vector<Rendezvous> rvs(groups);
+  auto group_of = [&](int b) { return (int)((long long)b * groups / B); };  // contiguous, equal (+-1) ranges
+  for (int g = 0; g < groups; ++g) {
+    rvs[g].sys = sys;
+    rvs[g].eval_mutex = &eval_mutex;
+    rvs[g].per = per;
+    rvs[g].batch = B;
+    rvs[g].x = &x_all;
+    rvs[g].grad = &grad_all;
+    rvs[g].scalars = &scalars_all;
+    rvs[g].diverged = &diverged_all;
+  }
+  for (int b = 0; b < B; ++b) ++rvs[group_of(b)].active;
   std::vector<ProblemCtx> ctx(B);
   std::vector<std::thread> threads;
   threads.reserve(B);
   for (int b = 0; b < B; ++b) {
+    Rendezvous& rv = rvs[group_of(b)];
     ctx[b].rv = &rv;
     ctx[b].id = b;
     auto body = [&, b] {
+      Rendezvous& mine = *ctx[b].rv;
       std::vector<double> x0(per), g(per);
       for (size_t e = 0; e < per; ++e)  // x0 = (target - q0)/T, registration.cpp:47-52
         x0[e] = (s->host_target[b * per + e] - s->host_q0[b * per + e]) / s->timesteps;
@@ -490,30 +544,36 @@ int lms_batch_register(lms_system* sys, const lms_lbfgs_params* params, double* 
         rc = code;
       }
       status[b] = rc;
-      std::unique_lock<std::mutex> lock(rv.m);
-      --rv.active;  // this problem no longer takes part in rounds
-      if (rv.failure == LMS_OK && rv.active > 0 && rv.submitted == rv.active) rv.run_round();
+      std::unique_lock<std::mutex> lock(mine.m);
+      --mine.active;  // this problem no longer takes part in rounds
+      if (mine.failure == LMS_OK && mine.active > 0 && mine.submitted == mine.active) mine.run_round();
     };
     try {
       threads.emplace_back(body);
     } catch (...) {  // std::system_error: no more threads.  Wake and fail the ones already running.
-      std::unique_lock<std::mutex> lock(rv.m);
-      rv.failure = LMS_ERR_STATE;
-      rv.cv.notify_all();
+      for (auto& r : rvs) {
+        std::unique_lock<std::mutex> lock(r.m);
+        r.failure = LMS_ERR_STATE;
+        r.cv.notify_all();
+      }
       break;
     }
   }
   for (auto& t : threads) t.join();
-  if (rounds_out) *rounds_out = rv.rounds;
-  if (rv.failure != LMS_OK) return rv.failure;
+  int rounds_total = 0;
+  for (auto& r : rvs) rounds_total += r.rounds;
+  if (rounds_out) *rounds_out = rounds_total;
+  for (auto& r : rvs)
+    if (r.failure != LMS_OK) return r.failure;
   if (warped_out) {
     // final re-integration under every p0* (registration.cpp:85-93): one more batched evaluation
     std::vector<int> ok;
     for (int b = 0; b < B; ++b)
       if (status[b] == LMS_OK) ok.push_back(b);
     if (!ok.empty()) {
-      int rc = lms_batch_eval(sys, ok.size(), ok.data(), momenta_out, rv.grad.data(), rv.scalars.data(),
-                              rv.diverged.data());
+      const bool all = (int)ok.size() == B;
+      int rc = lms_batch_eval(sys, ok.size(), all ? nullptr : ok.data(), momenta_out, grad_all.data(),
+                              scalars_all.data(), diverged_all.data());
       if (rc != LMS_OK) return rc;
     }
     return lms_batch_final_q(sys, warped_out);

@@ -192,7 +192,7 @@ class System final : public SystemBase {
   void final_q_batch(double* out) override;
   cudaStream_t stream_handle() const override { return stream_; }
   const double* staging_scratch() const override { return d_io_; }
-  const double* last_x_device() const override { return stored_t_ == timesteps && bound ? d_x_ : nullptr; }
+  const double* last_x_device() const override { return stored_t_ == timesteps && bound && d_x_current_ ? d_x_ : nullptr; }
 
  private:
   static constexpr int kState = 2 * D;  // planes per (q,p) or (alpha,beta) state
@@ -271,6 +271,7 @@ class System final : public SystemBase {
   unsigned long long* d_diverged_ = nullptr;
   double* d_io_ = nullptr;  // 4 x (n*D) doubles of conversion staging
   double* d_x_ = nullptr;
+  bool d_x_current_ = false;  // d_x_ holds the point of the last evaluation (not after a zero-copy host-buffer call)
   double* d_grad_ = nullptr;
   double* h_scalars_ = nullptr;  // pinned: 3 doubles + the divergence word
   double* d_metrics_ = nullptr;  // registration_metrics: {avg, max} before and after

@@ -894,10 +894,15 @@ void System<T, D>::eval_batch(const double* x, double* grad, double* scalars, in
     traj0_is_q0_ = true;
   }
   if (subset) {
-    for (int k = 0; k < count; ++k) {
+    for (int k = 0; k < count; ++k)
       if (ids[k] < 0 || ids[k] >= batch) throw StatusError{LMS_ERR_INVALID, "problem id out of range"};
-      LMS_CUDA(cudaMemcpyAsync(d_x_ + ids[k] * per, x + ids[k] * per, per * sizeof(double), cudaMemcpyHostToDevice,
-                               stream_));
+    // runs of neighbouring ids travel as one copy (the rendezvous of lms_batch_register hands sorted lists)
+    for (int k = 0; k < count;) {
+      int e = k + 1;
+      while (e < count && ids[e] == ids[e - 1] + 1) ++e;
+      LMS_CUDA(cudaMemcpyAsync(d_x_ + ids[k] * per, x + ids[k] * per, (size_t)(e - k) * per * sizeof(double),
+                               cudaMemcpyHostToDevice, stream_));
+      k = e;
     }
     LMS_CUDA(cudaMemcpyAsync(d_ids_, ids, count * sizeof(int), cudaMemcpyHostToDevice, stream_));
   } else {
@@ -912,9 +917,13 @@ void System<T, D>::eval_batch(const double* x, double* grad, double* scalars, in
   }
   LMS_CUDA(cudaEventRecord(ev_end_, stream_));
   if (subset) {
-    for (int k = 0; k < count; ++k)
-      LMS_CUDA(cudaMemcpyAsync(grad + ids[k] * per, d_grad_ + ids[k] * per, per * sizeof(double),
+    for (int k = 0; k < count;) {
+      int e = k + 1;
+      while (e < count && ids[e] == ids[e - 1] + 1) ++e;
+      LMS_CUDA(cudaMemcpyAsync(grad + ids[k] * per, d_grad_ + ids[k] * per, (size_t)(e - k) * per * sizeof(double),
                                cudaMemcpyDeviceToHost, stream_));
+      k = e;
+    }
   } else {
     LMS_CUDA(cudaMemcpyAsync(grad, d_grad_, per * batch * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   }
@@ -965,6 +974,7 @@ void System<T, D>::eval(const double* x, double* grad, double* scalars, bool dev
   if (zero_copy) {
     const size_t nd = (size_t)n() * D;
     std::memcpy(h_zc_, x, bytes);
+    d_x_current_ = false;
     LMS_CUDA(cudaEventRecord(ev_begin_, stream_));
     launch_small(/*host_io=*/true);
     LMS_CUDA(cudaEventRecord(ev_end_, stream_));
@@ -983,6 +993,7 @@ void System<T, D>::eval(const double* x, double* grad, double* scalars, bool dev
   } else {
     LMS_CUDA(cudaMemcpyAsync(d_x_, x, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                              stream_));
+    d_x_current_ = true;
     LMS_CUDA(cudaEventRecord(ev_begin_, stream_));
     if (use_small_ && !timed) {
       launch_small();
