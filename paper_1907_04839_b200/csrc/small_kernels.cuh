@@ -121,11 +121,33 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity)
 
 // All CTAs of the (cooperative) launch meet here.  Everything written before it -- by the generic proxy -- is
 // visible after it to generic loads that bypass L1 (__ldcg) and to bulk-async copies (async proxy).  `target` is
-// the counter value that means "everybody has arrived" (advanced by gridDim.x per barrier; wrap-safe compare).
+// the counter value that means "everybody has arrived" (wrap-safe compare).
+// Hierarchical when LMS_SMALL_CLUSTER_BARRIER is set: the CTAs of a cluster meet in the hardware cluster barrier,
+// ONE of them arrives at / polls the global counter (an eighth of the same-address atomics and pollers), and a
+// second cluster barrier releases the rest; release / acquire are cumulative, so the chain CTA -> cluster barrier ->
+// red.release.gpu -> ld.acquire.gpu -> cluster barrier -> CTA orders every CTA's writes before every CTA's reads.
+#ifndef LMS_SMALL_CLUSTER_BARRIER
+#define LMS_SMALL_CLUSTER_BARRIER 0
+#endif
 __device__ __forceinline__ void small_grid_barrier(unsigned* bar, unsigned& target)
 {
-  target += gridDim.x;
   asm volatile("fence.proxy.async.global;" ::: "memory");
+#if LMS_SMALL_CLUSTER_BARRIER
+  unsigned cl_rank, cl_size;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(cl_rank));
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(cl_size));
+  target += gridDim.x / cl_size;
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (cl_rank == 0 && threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+    } while ((int)(seen - target) < 0);
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+#else
+  target += gridDim.x;
   __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
@@ -135,6 +157,7 @@ __device__ __forceinline__ void small_grid_barrier(unsigned* bar, unsigned& targ
     } while ((int)(seen - target) < 0);
   }
   __syncthreads();
+#endif
   asm volatile("fence.proxy.async.global;" ::: "memory");  // before this thread's bulk-async reads of that data
 }
 
@@ -264,7 +287,7 @@ __device__ __forceinline__ SmallPlan small_plan(int n)
 
 // One time step for this CTA's rows.  MODE kFwd: state -> out = next snapshot (Euler, shooting.hpp:205-211) with
 // the first / last step extras; MODE kAdj: (state, adj_in) -> out = next adjoint state (:302-306).
-template <typename T, int D, int MODE>
+template <typename T, int D, int MODE, int RS>
 __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPlan& pl, const T* __restrict__ state,
                                            const T* __restrict__ adj_in, T* __restrict__ out, unsigned epi, int step_no,
                                            T* tile, T* part, T* rowbuf, unsigned long long* bars, unsigned& phase,
@@ -274,7 +297,6 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
   using S = Shape<MODE, D>;
   constexpr int NC = S::kColComps, NR = S::kRowComps, NA = S::kAcc;
   constexpr bool F32 = sizeof(T) == 4;
-  constexpr int RS = SmallShape<T>::kRowsPerSlot;
   constexpr int CH = SmallShape<T>::kChunk;
   constexpr int NTOT = SmallShape<T>::kCols;
   constexpr int GPC = CH / 32;  // 32-column groups per chunk
@@ -318,8 +340,7 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
     // ---- row operands of the CTA's rows: one value per thread (of the other warps), read past L1 (other CTAs wrote
     // them before the grid barrier) and parked in shared memory for the sweeps and the epilogue; the fetch
     // overlaps the chunk copies.  kSmallMaxSlots * RS * NR <= 384 values <= 15 warps ----
-    const int t = threadIdx.x;
-    if (t < pl.s_b * RS * NR) {
+    for (int t = threadIdx.x; t < pl.s_b * RS * NR; t += 32 * (kSmallWarps - 1)) {
       const int rl = t / NR, k = t - rl * NR;  // row of the CTA, component
       const long long row = (long long)pl.slot0 * RS + rl;
       // [slot][component][row of the slot]: a slot's packed (row 0, row 1) operand is one 8-byte word
@@ -331,7 +352,8 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
   const unsigned bars_u32 = smem_u32(bars);
 
   // ---- the warp's pieces: (slot, groups [g0, g1)) ----
-  constexpr int U = F32 ? (MODE == kAdj ? LMS_SMALL_UA : LMS_SMALL_UF) : (MODE == kAdj ? LMS_SMALL_UA64 : LMS_SMALL_UF64);
+  constexpr int U = F32 ? (MODE == kAdj ? (RS == 4 ? 1 : LMS_SMALL_UA) : (RS == 4 ? 2 : LMS_SMALL_UF))
+                        : (MODE == kAdj ? LMS_SMALL_UA64 : LMS_SMALL_UF64);
   int waited = 0;  // chunks [0, waited) have landed
 #pragma unroll 1
   for (int pc = 0; pc < pl.n_pieces; ++pc) {
@@ -339,30 +361,34 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
     const int g0 = pc ? pl.g0[1] : pl.g0[0];
     const int g1 = pc ? pl.g1[1] : pl.g1[0];
     T rv[RS][NR];  // warp-uniform
-    if constexpr (RS == 2) {
+    if constexpr (RS > 1) {
 #pragma unroll
       for (int k = 0; k < NR; ++k) {
-        T v[2];
-        load_cols<T, 2>(rowbuf + (sl * NRMAX + k) * 2, v);
-        rv[0][k] = v[0];
-        rv[1][k] = v[1];
+        T v[RS];
+        load_cols<T, RS>(rowbuf + (sl * NRMAX + k) * RS, v);
+#pragma unroll
+        for (int h = 0; h < RS; ++h) rv[h][k] = v[h];
       }
     } else {
 #pragma unroll
       for (int k = 0; k < NR; ++k) rv[0][k] = rowbuf[sl * NRMAX + k];
     }
 
+    constexpr int RPK = F32 ? RS / 2 : 1;  // packed row pairs per slot (fp32)
     T acc[NV];
-    float2 ri2[NR], acc2[NA];
+    float2 ri2[RPK][NR], acc2[RPK][NA];
     float2 kexp2, ns2, neg1;
     if constexpr (F32) {
 #pragma unroll
-      for (int k = 0; k < NR; ++k) {
-        const float lo = (float)rv[0][k], hi = (float)rv[RS - 1][k];
-        ri2[k] = k < D ? make_float2(-lo, -hi) : make_float2(lo, hi);  // pair_term_packed takes -q_i
-      }
+      for (int rp = 0; rp < RPK; ++rp) {
 #pragma unroll
-      for (int k = 0; k < NA; ++k) acc2[k] = make_float2(0.f, 0.f);
+        for (int k = 0; k < NR; ++k) {
+          const float lo = (float)rv[2 * rp][k], hi = (float)rv[2 * rp + 1][k];
+          ri2[rp][k] = k < D ? make_float2(-lo, -hi) : make_float2(lo, hi);  // pair_term_packed takes -q_i
+        }
+#pragma unroll
+        for (int k = 0; k < NA; ++k) acc2[rp][k] = make_float2(0.f, 0.f);
+      }
       kexp2 = splat2((float)a.kexp);
       ns2 = splat2(-(float)a.inv_sig2);
       neg1 = splat2(-1.f);
@@ -375,7 +401,8 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
         float2 cj2[NC];
 #pragma unroll
         for (int k = 0; k < NC; ++k) cj2[k] = splat2((float)cj[k]);
-        pair_term_packed<D, MODE>(ri2, cj2, acc2, kexp2, ns2, neg1);
+#pragma unroll
+        for (int rp = 0; rp < RPK; ++rp) pair_term_packed<D, MODE>(ri2[rp], cj2, acc2[rp], kexp2, ns2, neg1);
       } else {
         pair_term<T, D, MODE>(rv[0], cj, acc, a.kexp, a.inv_sig2, exp_tbl);
       }
@@ -428,11 +455,13 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
     // ---- the piece's sums over the lanes (fixed tree), parked for the slot's epilogue threads ----
     if constexpr (F32) {
 #pragma unroll
-      for (int k = 0; k < NA; ++k) {
-        const bool flip = MODE == kFwd && k < D;  // the packed forward term accumulates -(p_i.p_j) K dx
-        acc[k] = (T)(flip ? -acc2[k].x : acc2[k].x);
-        acc[(RS - 1) * NA + k] = (T)(flip ? -acc2[k].y : acc2[k].y);
-      }
+      for (int rp = 0; rp < RPK; ++rp)
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+          const bool flip = MODE == kFwd && k < D;  // the packed forward term accumulates -(p_i.p_j) K dx
+          acc[(2 * rp) * NA + k] = (T)(flip ? -acc2[rp][k].x : acc2[rp][k].x);
+          acc[(2 * rp + 1) * NA + k] = (T)(flip ? -acc2[rp][k].y : acc2[rp][k].y);
+        }
     }
     int first;
     unsigned live_mask;
@@ -502,11 +531,10 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
   }
 }
 
-template <typename T, int D>
+template <typename T, int D, int RS = SmallShape<T>::kRowsPerSlot>
 __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const SmallArgs<T> a)
 {
   constexpr int kThreadsHere = 32 * kSmallWarps;
-  constexpr int RS = SmallShape<T>::kRowsPerSlot;
   constexpr int NV = RS * 2 * D;
   extern __shared__ __align__(128) unsigned char small_smem[];
   T* tile = reinterpret_cast<T*>(small_smem);
@@ -553,7 +581,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const S
   // forward Euler flow, T+1 snapshots kept for the adjoint (shooting.hpp:199-212)
   for (int t = 0; t < Tn; ++t) {
     const unsigned epi = kEpiEuler | (t == 0 ? kEpiFirstStep : 0u) | (t == Tn - 1 ? kEpiLastStep : 0u);
-    small_step<T, D, kFwd>(a, pl, a.traj + (long long)t * a.snap_elems, nullptr, a.traj + (long long)(t + 1) * a.snap_elems,
+    small_step<T, D, kFwd, RS>(a, pl, a.traj + (long long)t * a.snap_elems, nullptr, a.traj + (long long)(t + 1) * a.snap_elems,
                            epi, t + 1, tile, part, rowbuf, bars, phase, hsum, msum, exp_tbl, 8 * t);
     LMS_TRACE_POINT(a, 8 * t + 4);
     if (t == Tn - 1) {
@@ -599,7 +627,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const S
   T* adj_in = a.adj0;
   T* adj_out = a.adj1;
   for (int t = Tn - 1; t >= 0; --t) {
-    small_step<T, D, kAdj>(a, pl, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
+    small_step<T, D, kAdj, RS>(a, pl, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
                            kEpiEuler | (t == 0 ? kEpiGradOut : 0u), t, tile, part, rowbuf, bars, phase, hsum, msum,
                            exp_tbl, 8 * (2 * Tn - 1 - t));
     LMS_TRACE_POINT(a, 8 * (2 * Tn - 1 - t) + 4);

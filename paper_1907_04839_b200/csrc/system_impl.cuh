@@ -390,10 +390,13 @@ void System<T, D>::plan_small()
 {
   use_small_ = false;
   if (!small_enabled_ || batch != 1 || comm_active_ || n() <= 0 || n() > small_max_n_) return;
-  constexpr int RS = SmallShape<T>::kRowsPerSlot;
   constexpr int CH = SmallShape<T>::kChunk;
   if (stride_ % CH != 0 || ceil_div(n(), CH) > SmallShape<T>::kMaxChunks) return;  // every chunk gets its own buffer
-  const int slots = ceil_div(n(), RS);
+  // rows per slot: one packed row pair in fp32, one row in fp64.  (Two packed pairs per slot -- every column load
+  // serving both, as in the tiled R = 4 kernels; the kernel template takes RS = 4 -- measured slower on the B200:
+  // N = 4000 0.504 vs 0.490 ms, N = 2000 0.188 vs 0.185 ms; it spills at the 128-register cap of a 512-thread CTA.)
+  const int rs = SmallShape<T>::kRowsPerSlot;
+  const int slots = ceil_div(n(), rs);
   const int grid = std::min(num_sms_, slots);
   // A CTA's slots x 32-column groups are dealt to its sixteen warps in equal contiguous runs (small_kernels.cuh),
   // so any slot count up to kSmallMaxSlots keeps every warp busy.  (Before: one slot per row warp, the spare warps
@@ -479,7 +482,8 @@ void System<T, D>::launch_small(bool host_io)
   a.diverged = d_diverged_;
   a.barrier = small_bar_;
   a.bar_base = small_bar_count_;
-  small_bar_count_ += (unsigned)small_grid_ * (unsigned)(2 * timesteps);  // 1 + T + (T-1) barriers per launch
+  // 1 + T + (T-1) barriers per launch; one arrival per CTA, or per cluster with the hierarchical barrier
+  small_bar_count_ += (unsigned)(LMS_SMALL_CLUSTER_BARRIER ? small_grid_ / small_cluster_ : small_grid_) * (unsigned)(2 * timesteps);
 #ifdef LMS_SMALL_TRACE
   a.trace = reinterpret_cast<unsigned long long*>(d_io_);  // staging scratch: idle during an evaluation
 #else
