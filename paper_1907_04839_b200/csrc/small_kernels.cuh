@@ -355,8 +355,11 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
   constexpr int U = F32 ? (MODE == kAdj ? (RS == 4 ? 1 : LMS_SMALL_UA) : (RS == 4 ? 2 : LMS_SMALL_UF))
                         : (MODE == kAdj ? LMS_SMALL_UA64 : LMS_SMALL_UF64);
   int waited = 0;  // chunks [0, waited) have landed
+  // A run that wraps from the tail of one slot into the head of the next is swept head first: the head starts at
+  // column 0, whose chunk lands first, while the tail's chunks are the last to arrive (a warp waits only for the
+  // chunks it reads).  The epilogue adds a slot's pieces in ascending column order whatever order they were swept in.
 #pragma unroll 1
-  for (int pc = 0; pc < pl.n_pieces; ++pc) {
+  for (int pc = pl.n_pieces - 1; pc >= 0; --pc) {
     const int sl = pc ? pl.sl[1] : pl.sl[0];
     const int g0 = pc ? pl.g0[1] : pl.g0[0];
     const int g1 = pc ? pl.g1[1] : pl.g1[0];

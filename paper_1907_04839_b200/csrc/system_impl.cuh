@@ -252,7 +252,15 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   // round trip per few segments).  Measured on B200 (N = 5000: 0.795 -> 0.727 ms, N = 7000: 1.240 -> 1.213 ms per
   // gradient): beyond ~20 segments the serial chain costs more than the occupancy it buys, down to 2 CTAs per SM
   // (N = 20 000 runs only 3.5 % slower at 3 CTAs per SM than at 7).
-  p.grid = (int)std::min<long long>(p.grid, std::max<long long>(2LL * num_sms_, 20LL * p.n_row_tiles));
+  static const int seg_cap = [] {
+    const char* e = std::getenv("LMS_SEG_CAP");  // experiment knob: partial segments per row tile at most
+    return e ? std::max(std::atoi(e), 1) : 20;
+  }();
+  static const int seg_floor = [] {
+    const char* e = std::getenv("LMS_SEG_FLOOR_CTAS_PER_SM");  // experiment knob: never fewer CTAs per SM than this
+    return e ? std::max(std::atoi(e), 1) : 2;
+  }();
+  p.grid = (int)std::min<long long>(p.grid, std::max<long long>((long long)seg_floor * num_sms_, (long long)seg_cap * p.n_row_tiles));
   // mid-size problems: a whole number of CTAs per SM, so no SM carries one CTA more than its neighbours
   static const int round_from = [] {
     const char* e = std::getenv("LMS_ROUND_FROM");  // experiment knob: round only grids of at least this many CTAs per SM
