@@ -103,12 +103,17 @@ struct PairArgs {
   long long peer_delta[kMaxPeers];  // byte distance from this rank's arena to each peer's mapping of its arena
 };
 
-// One value to the local buffer and to the same place in every peer's arena.
-template <typename T, typename V>
+// One value to the local buffer and -- PEERS kernels only -- to the same place in every peer's arena.  (The peer loop
+// is compiled only into the kernels a row-partitioned handle launches with the peer-push transport: unrolled into
+// every epilogue store it made the kernels 4-5 x larger -- 11 584 instead of 2 200 instructions for the fp32 adjoint --
+// and the cold, bloated epilogue cost every launch of a single-GPU evaluation 0.3 % at N = 20 000 up to 6 % at N = 1000.)
+template <bool PEERS, typename T, typename V>
 __device__ __forceinline__ void put_all(const PairArgs<T>& a, V* p, V v)
 {
   *p = v;
-  for (int k = 0; k < a.n_peers; ++k) *reinterpret_cast<V*>(reinterpret_cast<char*>(p) + a.peer_delta[k]) = v;
+  if constexpr (PEERS) {
+    for (int k = 0; k < a.n_peers; ++k) *reinterpret_cast<V*>(reinterpret_cast<char*>(p) + a.peer_delta[k]) = v;
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -504,7 +509,7 @@ __device__ __forceinline__ double block_sum(double v, double* scratch)
 // its sums in its own tile buffers, rank 0 adds the kClusterSize copies in ascending column order and runs the
 // epilogue) instead of going through global slots, a fence, an arrival counter and L2 round trips.
 template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false,
-          bool AOS = false, bool CLUSTER = false>
+          bool AOS = false, bool CLUSTER = false, bool PEERS = false>
 __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> a)
 {
   static_assert(!CLUSTER || 2 * Shape<MODE, D>::kColComps * kTileJ >= Shape<MODE, D>::kAcc * kThreads * R,
@@ -857,8 +862,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
                 qn[k] = Math<T>::add_rn(ri[r][k], Math<T>::mul_rn(a.dt, hp[k]));
                 const T pn = Math<T>::add_rn(ri[r][D + k], -Math<T>::mul_rn(a.dt, hq[k]));
                 ok = ok && Math<T>::finite(qn[k]) && Math<T>::finite(pn);
-                put_all(a, &out_b[(long long)k * a.ostride + row], qn[k]);
-                put_all(a, &out_b[(long long)(D + k) * a.ostride + row], pn);
+                put_all<PEERS>(a, &out_b[(long long)k * a.ostride + row], qn[k]);
+                put_all<PEERS>(a, &out_b[(long long)(D + k) * a.ostride + row], pn);
               }
               if (!ok) atomicMin(diverged_b, ((unsigned long long)(unsigned)a.step << 32) | 0xffffffffull);
               if (a.epi & kEpiFirstStep) {
@@ -875,8 +880,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
                   const double df = (double)qn[k] - (double)tg;  // shooting.hpp:324-325
                   msum += df * df;
                   // alpha_T = 2*lambda*(q(1) - target), beta_T = 0   (shooting.hpp:290-296)
-                  put_all(a, &adj_seed_b[(long long)k * a.ostride + row], Math<T>::mul_rn(a.two_lambda, qn[k] - tg));
-                  put_all(a, &adj_seed_b[(long long)(D + k) * a.ostride + row], T(0));
+                  put_all<PEERS>(a, &adj_seed_b[(long long)k * a.ostride + row], Math<T>::mul_rn(a.two_lambda, qn[k] - tg));
+                  put_all<PEERS>(a, &adj_seed_b[(long long)(D + k) * a.ostride + row], T(0));
                 }
               }
             } else {
@@ -898,10 +903,10 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
                 // alpha += dt*d_alpha ; beta += dt*d_beta   (shooting.hpp:302-306)
                 const T an = Math<T>::add_rn(ri[r][2 * D + k], Math<T>::mul_rn(a.dt, da));
                 const T bn = Math<T>::add_rn(ri[r][3 * D + k], Math<T>::mul_rn(a.dt, dbeta));
-                put_all(a, &out_b[(long long)k * a.ostride + row], an);
-                put_all(a, &out_b[(long long)(D + k) * a.ostride + row], bn);
+                put_all<PEERS>(a, &out_b[(long long)k * a.ostride + row], an);
+                put_all<PEERS>(a, &out_b[(long long)(D + k) * a.ostride + row], bn);
                 if (a.epi & kEpiGradOut)  // grad = beta_0 + hp(q0,p0)   (shooting.hpp:311-313)
-                  put_all(a, &grad_out_b[row * D + k],
+                  put_all<PEERS>(a, &grad_out_b[row * D + k],
                           (double)Math<T>::add_rn(bn, hp0_b[(long long)k * a.ostride + row]));
               } else {
                 out_b[(long long)k * a.ostride + row] = da;
@@ -915,11 +920,11 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         // block-uniform flags: every thread takes the same branch around the barriers in block_sum
         if (a.epi & kEpiFirstStep) {
           const double h = block_sum(hsum, red_scratch);
-          if (tid == 0) put_all(a, &h_part_b[(long long)rt * R], h);  // indexed in 128-row units
+          if (tid == 0) put_all<PEERS>(a, &h_part_b[(long long)rt * R], h);  // indexed in 128-row units
         }
         if (a.epi & kEpiLastStep) {
           const double m = block_sum(msum, red_scratch);
-          if (tid == 0) put_all(a, &mm_part_b[(long long)rt * R], m);
+          if (tid == 0) put_all<PEERS>(a, &mm_part_b[(long long)rt * R], m);
         }
       }
     }

@@ -125,17 +125,19 @@ template <typename T>
 struct KernelChoice {
   void (*fn)(PairArgs<T>) = nullptr;
   void (*fn_cluster)(PairArgs<T>) = nullptr;  // same shape with the cluster combine (small problems), or null
+  void (*fn_peers)(PairArgs<T>) = nullptr;    // same shape with the peer-push stores in its epilogues (row partition), or null
   int rows_per_thread = 0;
   const char* name = "";
 };
 
 template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false,
-          bool AOS = false, bool WITH_CLUSTER = false>
+          bool AOS = false, bool WITH_CLUSTER = false, bool WITH_PEERS = false>
 KernelChoice<T> make_choice(const char* name)
 {
   KernelChoice<T> c;
   c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS>;
   if constexpr (WITH_CLUSTER) c.fn_cluster = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, true>;
+  if constexpr (WITH_PEERS) c.fn_peers = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, false, true>;
   c.rows_per_thread = R;
   c.name = name;
   return c;

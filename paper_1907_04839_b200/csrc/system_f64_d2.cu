@@ -6,12 +6,12 @@ namespace lms {
 template <>
 KernelChoice<double> pick_kernel<double, 2, kFwd>(int)
 {
-  return make_choice<double, 2, kFwd, 2, 2, 3>("fwd_f64_d2_r2_j2");
+  return make_choice<double, 2, kFwd, 2, 2, 3, false, 1, false, false, false, true>("fwd_f64_d2_r2_j2");
 }
 template <>
 KernelChoice<double> pick_kernel<double, 2, kAdj>(int)
 {
-  return make_choice<double, 2, kAdj, 2, 2, 2>("adj_f64_d2_r2_j2");
+  return make_choice<double, 2, kAdj, 2, 2, 2, false, 1, false, false, false, true>("adj_f64_d2_r2_j2");
 }
 template <>
 KernelChoice<double> pick_kernel<double, 2, kVel>(int)

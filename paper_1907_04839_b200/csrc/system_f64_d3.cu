@@ -9,7 +9,7 @@ KernelChoice<double> pick_kernel<double, 3, kFwd>(int v)
   switch (v) {
     case 1: return make_choice<double, 3, kFwd, 1, 2, 4>("fwd_f64_r1_j2");
     case 5: return make_choice<double, 3, kFwd, 2, 2, 3, false, 2>("fwd_f64_r2_j2_u2");
-    default: return make_choice<double, 3, kFwd, 2, 2, 3, false, 2, true>("fwd_f64_r2_j2_u2_tma");
+    default: return make_choice<double, 3, kFwd, 2, 2, 3, false, 2, true, false, false, true>("fwd_f64_r2_j2_u2_tma");
   }
 }
 template <>
@@ -18,7 +18,7 @@ KernelChoice<double> pick_kernel<double, 3, kAdj>(int v)
   switch (v) {
     case 1: return make_choice<double, 3, kAdj, 1, 2, 3>("adj_f64_r1_j2");
     case 5: return make_choice<double, 3, kAdj, 2, 2, 2, false, 2>("adj_f64_r2_j2_u2");
-    default: return make_choice<double, 3, kAdj, 2, 2, 2, false, 2, true>("adj_f64_r2_j2_u2_tma");
+    default: return make_choice<double, 3, kAdj, 2, 2, 2, false, 2, true, false, false, true>("adj_f64_r2_j2_u2_tma");
   }
 }
 template <>

@@ -358,6 +358,13 @@ void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchP
     throw StatusError{LMS_ERR_STATE, "launch plan outgrew the stream-K partial buffers"};
   a.partials = partials_;
   a.counters = counters_;
+  // the peer-push stores exist only in the PEERS instantiation of a shape (pair_kernels.cuh, put_all)
+  auto fn = k.fn;
+  if (a.n_peers > 0) {
+    if (k.fn_peers == nullptr)
+      throw StatusError{LMS_ERR_STATE, "this kernel variant has no peer-push instantiation (use the default variant)"};
+    fn = k.fn_peers;
+  }
   if (plan.cluster) {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(plan.grid);
@@ -384,9 +391,9 @@ void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchP
     at[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    LMS_CUDA(cudaLaunchKernelEx(&lc, k.fn, a));
+    LMS_CUDA(cudaLaunchKernelEx(&lc, fn, a));
   } else {
-    k.fn<<<plan.grid, kThreads, 0, stream_>>>(a);
+    fn<<<plan.grid, kThreads, 0, stream_>>>(a);
     LMS_CUDA(cudaGetLastError());
   }
   ++last_eval_launches;
@@ -1411,6 +1418,19 @@ void System<T, D>::p2p_connect(const unsigned char* blobs)
   local_ = nullptr;
   p2p_active_ = world_ > 1;
   comm_active_ = world_ > 1;
+  // The peer-push instantiations are launched for the first time inside a partitioned evaluation, when a peer's
+  // stream may already sit in a stream-ordered wait for this rank's flag: lazy module loading at that point
+  // synchronises the context and would deadlock ranks that share one.  Load them now.
+  void (*const peer_fns[2])(PairArgs<T>) = {k_fwd_.fn_peers, k_adj_.fn_peers};
+  for (auto fn : peer_fns) {
+    if (fn == nullptr) throw StatusError{LMS_ERR_STATE, "this kernel variant has no peer-push instantiation (use the default variant)"};
+    cudaFuncAttributes attr;
+    LMS_CUDA(cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(fn)));
+    PairArgs<T> none{};  // no row tiles, no columns: the kernel starts and returns without touching memory
+    fn<<<1, kThreads, 0, stream_>>>(none);
+    LMS_CUDA(cudaGetLastError());
+  }
+  sync();
 }
 
 template <typename T, int D>
