@@ -404,6 +404,9 @@ struct PinnedDoubles {  // staging the device copies read / write directly (page
   double* p = nullptr;
   size_t n = 0;
   bool pinned = false;
+  PinnedDoubles() = default;
+  PinnedDoubles(const PinnedDoubles&) = delete;
+  PinnedDoubles& operator=(const PinnedDoubles&) = delete;
   void assign(size_t count)
   {
     n = count;

@@ -109,7 +109,14 @@ void System<T, D>::pick_kernels(bool partitioned)
 {
   int variant = cfg.variant;
   // (populations: the same shapes once the batch as a whole is that large -- 128 x N = 2000: 10.81 -> 10.49 ms)
-  const bool large = batch == 1 ? cfg.n >= 16000 : (cfg.n >= 1024 && (long long)batch * (long long)cfg.n >= 32000);
+  // Single problems: four rows per thread are 1-2 % faster per gradient from N = 8000 on and 3-4 % from 16 000 on, but their
+  // 512-row tiles pad more (N = 11 000: 2.4 % against 0.07 % for 256-row tiles).  Padding-aware: take them when the
+  // gain exceeds the extra padding (measured on B200, scripts/gpu_thresh.py: R = 4 / R = 2 ratio 0.98-0.99 at
+  // N = 8000-15 000 except 1.014 at 11 000; 1.01-1.13 below 8000).
+  auto padding = [&](long long rows) { return (double)round_up((long long)cfg.n, rows) / (double)std::max(cfg.n, (size_t)1) - 1.0; };
+  const double gain4 = cfg.n >= 16000 ? 0.035 : 0.015;
+  const bool large = batch == 1 ? (cfg.n >= 8000 && padding(4 * kThreads) - padding(2 * kThreads) < gain4)
+                                : (cfg.n >= 1024 && (long long)batch * (long long)cfg.n >= 32000);
   if (variant == 0 && sizeof(T) == 4 && large) variant = 25;
   k_fwd_ = pick_kernel<T, D, kFwd>(variant);
   k_adj_ = pick_kernel<T, D, kAdj>(variant);
