@@ -57,6 +57,36 @@ __global__ void __launch_bounds__(256) k(float* out, long long* cycles, float a,
   if (r == 123.456f) out[0] = r;
 }
 
+// fp64: DFMA operand forms (16 DP lanes per SMSP: 2.0 cycles per warp instruction is the pipe's own rate)
+template <int MODE>
+__global__ void __launch_bounds__(256) kd(double* out, long long* cycles, double a, double b)
+{
+  double acc[16], x[4], y[4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = threadIdx.x * 1e-3 + i;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { x[i] = a + i * 1e-3 * threadIdx.x; y[i] = b - i * 1e-3 * threadIdx.x; }
+  long long t0 = clock64();
+  for (int it = 0; it < ITER; ++it) {
+    if constexpr (MODE == 0) {  // acc += x * (uniform)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = fma(x[i & 3], b, acc[i]);
+    } else if constexpr (MODE == 1) {  // acc += x * y: three distinct register sources
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = fma(x[i & 3], y[(i >> 2) & 3], acc[i]);
+    } else {  // acc = acc * (uniform) + (uniform): one register source
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = fma(acc[i], a, b);
+    }
+  }
+  long long t1 = clock64();
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r += acc[i];
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+  if (r == 123.456) out[0] = r;
+}
+
 int main()
 {
   cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
@@ -74,12 +104,16 @@ int main()
     long long cmax = 0; for (auto c : cyc) cmax = c > cmax ? c : cmax;
     // 8 warps per SMSP (4 CTAs x 8 warps / 4 SMSPs)
     double per = (double)cmax / (ITER * 8.0 * (ffma2_per_iter > 0 ? ffma2_per_iter : 1.0));
-    printf("{\"name\": \"%s\", \"smsp_cycles_per_%s\": %.3f}\n", name, ffma2_per_iter > 0 ? "ffma2" : "iteration_per_warp", per);
+    printf("{\"name\": \"%s\", \"smsp_cycles_per_%s\": %.3f}\n", name, ffma2_per_iter > 0 ? "instruction" : "iteration_per_warp", per);
   };
   run("ffma2_x64_UR32_acc64 (4 words)", [&] { k<0><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f, d_src); }, 16);
   run("ffma2_x64_R32_acc64 from LDS (5 words)", [&] { k<1><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f, d_src); }, 16);
   run("ffma2_x64_UR32_acc64 via REDUX of the LDS value", [&] { k<2><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f, d_src); }, 16);
   run("ffma2_x64_y64_acc64 (6 words)", [&] { k<3><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f, d_src); }, 16);
   run("redux_x4_per_iteration", [&] { k<4><<<grid, 256>>>(d_out, d_cyc, 1.0001f, 0.5f, d_src); }, 0);
+  double* d_out64; CK(cudaMalloc(&d_out64, 8));
+  run("dfma_x_UR_acc (2 register sources)", [&] { kd<0><<<grid, 256>>>(d_out64, d_cyc, 1.0001, 0.5); }, 16);
+  run("dfma_x_y_acc (3 register sources)", [&] { kd<1><<<grid, 256>>>(d_out64, d_cyc, 1.0001, 0.5); }, 16);
+  run("dfma_acc_UR_UR (1 register source)", [&] { kd<2><<<grid, 256>>>(d_out64, d_cyc, 1.0001, 0.5); }, 16);
   return 0;
 }
