@@ -92,6 +92,31 @@ def test_batched_registrations_match_single_runs(prec):
         assert res.final_loss[b] < res.initial_loss[b]
 
 
+@pytest.mark.parametrize("groups", [1, 2, 3])
+def test_batch_register_in_alternating_groups(groups, monkeypatch):
+    """From 32 problems on lms_batch_register evaluates the population in alternating groups (the host L-BFGS
+    arithmetic of one group overlaps the device round of the other).  Every problem still runs the unchanged driver
+    on its own evaluations: whatever the group count, fp64 results agree with single registrations to rounding and
+    the rounds are coalesced per group."""
+    from paper_1907_04839_b200 import BatchedRegistrations, LbfgsParams, ShootingConfig, register_landmarks
+
+    monkeypatch.setenv("LMS_BATCH_GROUPS", str(groups))
+    batch, n, T, lam, iters = 34, 120, 4, 1e3, 8
+    q0, _, target = make_batch(batch, n, 77)
+    br = BatchedRegistrations(SIGMA, n, batch, 3, "f64", max_timesteps=T)
+    br.bind(q0, target, lam, T)
+    res = br.register(LbfgsParams(max_iter=iters))
+    br.close()
+    assert (res.status == 0).all()
+    assert res.rounds <= groups * (res.evaluations.max() + 1) and res.rounds < res.evaluations.sum()
+    for b in (0, 11, 16, 17, 33):  # first / last problems of the groups
+        one = register_landmarks(q0[b], target[b], ShootingConfig(sigma=SIGMA, timesteps=T, lam=lam, max_iter=iters,
+                                                                  precision="f64"))
+        assert res.iterations[b] == one.iterations and res.evaluations[b] == one.evaluations
+        assert res.final_loss[b] == pytest.approx(one.final_loss, rel=1e-8)
+        assert np.abs(res.warped[b] - one.warped).max() <= 1e-6
+
+
 def test_batch_handle_rejects_single_problem_calls():
     from paper_1907_04839_b200 import BatchedRegistrations, StateError, _lib
     import ctypes

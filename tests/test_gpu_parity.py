@@ -535,6 +535,42 @@ def test_registration_metrics_on_device(hs, oracle, prec, n, dim):
     s.close()
 
 
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("n", [700, 6000])
+def test_host_and_device_buffer_calls_agree(hs, prec, n):
+    """lms_objective_eval (host buffers; the persistent kernel reads / writes them in place through mapped pinned
+    memory) and lms_objective_eval_device (x / grad in HBM) are the same evaluation: bitwise equal loss, H, mismatch
+    and gradient, in either order, for a persistent-size and a tiled-size problem; a non-finite x is DivergedError(0)
+    through both."""
+    import torch
+
+    from paper_1907_04839_b200 import DivergedError
+
+    q, p, target, *_ = synth_case(n, 3, 900 + n, spread=7.0 * max(1.0, (n / 500.0) ** (1.0 / 3)))
+    s = hs(n, 3, prec, max_t=6)
+    s.bind_registration(q, target, 40.0, 6)
+    x = np.ascontiguousarray(p.ravel())
+    xd = torch.from_numpy(x).cuda()
+    gd = torch.empty_like(xd)
+    loss_h, grad_h = s.objective(x)
+    kin_h, mm_h = s.last_kinetic, s.last_mismatch
+    loss_d, kin_d, mm_d = s.objective_ptrs(xd.data_ptr(), gd.data_ptr(), device=True)
+    assert (loss_d, kin_d, mm_d) == (loss_h, kin_h, mm_h)
+    assert np.array_equal(gd.cpu().numpy(), grad_h)
+    loss_h2, grad_h2 = s.objective(x)  # and back: nothing of the device call leaks into the host call
+    assert loss_h2 == loss_h and np.array_equal(grad_h2, grad_h)
+    bad = x.copy()
+    bad[5] = np.inf
+    with pytest.raises(DivergedError) as e:
+        s.objective(bad)
+    assert e.value.timestep == 0
+    with pytest.raises(DivergedError) as e:
+        s.objective_ptrs(torch.from_numpy(bad).cuda().data_ptr(), gd.data_ptr(), device=True)
+    assert e.value.timestep == 0
+    loss_h3, _ = s.objective(x)  # the handle recovers
+    assert loss_h3 == loss_h
+
+
 def test_reference_minimize_drives_cuda_objective_through_cpp_adapter():
     """Drop-in check: the reference's UNMODIFIED minimize (lbfgs.cpp compiled in place into
     oracle/_ref/libref_cuda_driver.so) calls the CUDA objective through include/lmshoot_b200/objective.hpp.
