@@ -260,7 +260,10 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   // gradient): beyond ~20 segments the serial chain costs more than the occupancy it buys, down to 2 CTAs per SM
   // (N = 20 000 runs only 3.5 % slower at 3 CTAs per SM than at 7).
   static const int seg_cap = [] {
-    const char* e = std::getenv("LMS_SEG_CAP");  // experiment knob: partial segments per row tile at most
+    // experiment knobs: partial segments per row tile at most (LMS_SEG_CAP, or per kernel mode LMS_SEG_CAP_FWD / _ADJ / _VEL)
+    const char* mode_knob = MODE == kFwd ? "LMS_SEG_CAP_FWD" : (MODE == kAdj ? "LMS_SEG_CAP_ADJ" : "LMS_SEG_CAP_VEL");
+    const char* e = std::getenv(mode_knob);
+    if (!e) e = std::getenv("LMS_SEG_CAP");
     return e ? std::max(std::atoi(e), 1) : 20;
   }();
   static const int seg_floor = [] {
