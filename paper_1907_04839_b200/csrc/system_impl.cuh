@@ -1208,6 +1208,19 @@ void System<T, D>::relayout_for_world(int world, int rank)
   if (world > 1) {
     pick_kernels(/*partitioned=*/true);
     alloc_partials();
+    // Every kernel a partitioned evaluation launches is loaded now: with lazy module loading a first launch inside
+    // an evaluation can synchronise the context while a peer's stream sits in a stream-ordered wait for this
+    // rank (ranks that share one process and one GPU would deadlock; see p2p_connect).
+    const void* fns[] = {reinterpret_cast<const void*>(k_fwd_.fn), reinterpret_cast<const void*>(k_adj_.fn),
+                         reinterpret_cast<const void*>(k_fwd_.fn_peers), reinterpret_cast<const void*>(k_adj_.fn_peers),
+                         reinterpret_cast<const void*>(&publish_diverged<0>), reinterpret_cast<const void*>(&min_diverged<0>),
+                         reinterpret_cast<const void*>(&finalize_scalars<0>), reinterpret_cast<const void*>(&aos_to_planes<T>),
+                         reinterpret_cast<const void*>(&copy_planes<T>)};
+    for (const void* fn : fns) {
+      if (fn == nullptr) continue;
+      cudaFuncAttributes attr;
+      LMS_CUDA(cudaFuncGetAttributes(&attr, fn));
+    }
   }
   const long long new_stride = world > 1 ? partition_rows((long long)cfg.n, world, rank).stride : stride_;
   if (new_stride != stride_) {
