@@ -233,9 +233,8 @@ class System final : public SystemBase {
 
   cudaStream_t stream_ = nullptr;
   int num_sms_ = 0;
-  // programmatic dependent launch between the pair kernels: opt-in (LMS_PDL=1).  Measured on B200 inside the
-  // evaluation graph: no gain at N >= 10 000 (8.088 vs 8.085 ms) and a loss at N = 2000..5000 (0.28 vs 0.25 ms),
-  // where the early-scheduled CTAs of the next step compete with the running one.
+  // programmatic dependent launch between the pair kernels (see the constructor): on for single unpartitioned
+  // problems below 8000 landmarks since round 2 (a loss in round 1, when the kernels were 4-5 x larger); LMS_PDL overrides
   bool pdl_ = false;
   // cluster combine for small single problems (pair_kernel<..., CLUSTER>): opt-in with LMS_CLUSTER=1.  It is worth
   // 8-12 % below N = 1500 in fp32 (plan_for), but it changes the summation order of those sizes (the partitioned and
