@@ -80,6 +80,7 @@ struct PairArgs {
   unsigned long long* diverged;  // atomicMin of (step << 32 | point)
   // stream-K bookkeeping
   T* partials;   // 2 * gridDim.x slots of kAcc * (kThreads * R) sums (see the combine in pair_kernel)
+  int combine_smem_segments;  // partial segments the launch's dynamic shared memory holds at once (0: none)
   int* counters; // gridDim.x arrival counters, zero between launches
   // constants, rounded on the host exactly as the reference rounds them (shooting.hpp:63-68,114-115,
   // 196,293): kexp = k_scale * log2(e) for float (ex2.approx), k_scale * log2(e) * 2^kExpBits for double (Math<double>).
@@ -528,6 +529,9 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
   __shared__ double exp_tbl_all[sizeof(T) == 8 ? kExpTableDoubles : 1];  // fp64 only: 2^(j/2^B)
   __shared__ int s_last;
   __shared__ __align__(8) unsigned long long tile_bar[2];  // BULK only: one mbarrier per tile buffer
+  __shared__ __align__(8) unsigned long long combine_bar;  // the combine's bulk copies (see below)
+  extern __shared__ __align__(128) unsigned char combine_smem[];  // landing zone for partial segments, if any
+  unsigned combine_parity = 0;
   // Programmatic dependent launch: the next launch of the evaluation may start scheduling its CTAs as soon as
   // every CTA of this one is running, so they take over SM slots as ours retire and the launch latency
   // between the 2T dependent steps disappears.  A no-op when the launch carries no PDL attribute.
@@ -538,6 +542,13 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     if (threadIdx.x == 0) {
       mbar_init(&tile_bar[0], 1);
       mbar_init(&tile_bar[1], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
+  if (a.combine_smem_segments > 0) {
+    if (threadIdx.x == 0) {
+      mbar_init(&combine_bar, 1);
       mbar_fence_init();
     }
     __syncthreads();
@@ -810,13 +821,44 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         const long long first_start = cells * cta_first / G;
         const T* seg0 = a.partials + (2LL * cta_first) * (long long)(NA * BM);
         const long long first_off = first_start < cell_lo ? (long long)(NA * BM) : 0;
+        if (a.combine_smem_segments > 0 && !CLUSTER) {
+          // The launch has dynamic shared memory to spare (mid-size problems run two CTAs per SM): the segments land
+          // there by bulk-async copies, a batch per round trip instead of four segments per round trip through
+          // registers, and are added from shared memory in the same ascending order (bitwise the same sums).  The
+          // partial sums were written through the generic proxy: fence before the async proxy reads them.
+          T* land = reinterpret_cast<T*>(combine_smem);
+          const int per_batch = a.combine_smem_segments;
+          for (int base = 0; base < nseg; base += per_batch) {
+            const int cnt = nseg - base < per_batch ? nseg - base : per_batch;
+            if (tid == 0) {
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              mbar_expect_tx(&combine_bar, (unsigned)(cnt * NA * BM * sizeof(T)));
+              for (int s2 = 0; s2 < cnt; ++s2) {
+                const int ord = base + s2;
+                const T* theirs = seg0 + (long long)ord * (2 * NA * BM) + (ord == 0 ? first_off : 0);
+                bulk_g2s(land + (long long)s2 * (NA * BM), theirs, (unsigned)(NA * BM * sizeof(T)), &combine_bar);
+              }
+            }
+            mbar_wait(&combine_bar, combine_parity);
+            combine_parity ^= 1u;
+            for (int s2 = 0; s2 < cnt; ++s2) {
+              const T* theirs = land + (long long)s2 * (NA * BM);
+#pragma unroll
+              for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int k = 0; k < NA; ++k) acc[r][k] += theirs[k * BM + r * kThreads + tid];
+            }
+            __syncthreads();  // the landing zone is reused by the next batch (and by this CTA's next shared tile)
+          }
+        } else {
 #pragma unroll kCombineUnroll
-        for (int ord = 0; ord < nseg; ++ord) {
-          const T* theirs = seg0 + (long long)ord * (2 * NA * BM) + (ord == 0 ? first_off : 0);
+          for (int ord = 0; ord < nseg; ++ord) {
+            const T* theirs = seg0 + (long long)ord * (2 * NA * BM) + (ord == 0 ? first_off : 0);
 #pragma unroll
-          for (int r = 0; r < R; ++r)
+            for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int k = 0; k < NA; ++k) acc[r][k] += __ldcg(theirs + k * BM + r * kThreads + tid);
+              for (int k = 0; k < NA; ++k) acc[r][k] += __ldcg(theirs + k * BM + r * kThreads + tid);
+          }
         }
       }
     }

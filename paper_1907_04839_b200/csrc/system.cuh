@@ -165,6 +165,8 @@ struct LaunchPlan {
   bool cluster = false;  // launch fn_cluster as clusters of kClusterSize CTAs, one cluster per row tile
   int bm = 0;
   size_t partial_elems = 0;
+  int combine_segments = 0;  // partial segments the combine lands in dynamic shared memory per round trip (0: registers)
+  size_t dyn_smem = 0;       // dynamic shared memory of the launch (the combine's landing zone)
 };
 
 template <typename T, int D>
