@@ -151,6 +151,27 @@ def test_persistent_kernel_edge_sizes(hs, oracle, prec, dim, n):
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("n", [4500, 6100, 8200, 11000])
+def test_mid_size_parity(hs, oracle, prec, n):
+    """Mid-size single problems, where the launch machinery differs from both ends of the range: programmatic
+    dependent launch between the pair kernels (below 8000 landmarks), the combine's shared-memory landing zone (at
+    most two CTAs per SM, up to 20 partial segments per row tile), two-row shapes below 8000, four-row shapes above
+    unless they pad more than they gain (11 000).  Against the oracle, and bitwise run to run."""
+    tol = TOL[prec]
+    T, lam = 3, 50.0
+    q, p, target, *_ = synth_case(n, 3, 5000 + n, spread=7.0 * (n / 500.0) ** (1.0 / 3))
+    s = hs(n, 3, prec, max_t=4)
+    r = s.compute_gradient(q, p, target, lam, T)
+    assert s.last_eval_kernel_launches() == 2 * T + 2
+    loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, SIGMA, lam, T)
+    assert r.loss == pytest.approx(loss, rel=tol) and r.kinetic == pytest.approx(kin, rel=tol)
+    assert r.mismatch == pytest.approx(mm, rel=tol)
+    assert rel_inf(r.grad, grad) <= tol
+    again = s.compute_gradient(q, p, target, lam, T)
+    assert again.loss == r.loss and np.array_equal(again.grad, r.grad)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
 def test_two_dimensional_landmarks(hs, oracle, prec):
     tol = TOL[prec]
     q, p, target, alpha, beta = synth_case(300, 2, 7, spread=5.0)
