@@ -236,7 +236,7 @@ class System final : public SystemBase {
   cudaStream_t stream_ = nullptr;
   int num_sms_ = 0;
   // programmatic dependent launch between the pair kernels (see the constructor): on for single unpartitioned
-  // problems below 8000 landmarks since round 2 (a loss in round 1, when the kernels were 4-5 x larger); LMS_PDL overrides
+  // problems of 2400 to 8000 landmarks since round 2 (a loss in round 1, when the kernels were 4-5 x larger); LMS_PDL overrides
   bool pdl_ = false;
   // cluster combine for small single problems (pair_kernel<..., CLUSTER>): opt-in with LMS_CLUSTER=1.  It is worth
   // 8-12 % below N = 1500 in fp32 (plan_for), but it changes the summation order of those sizes (the partitioned and

@@ -48,9 +48,10 @@ System<T, D>::System(const lms_config& c, int batch_count)
   // Programmatic dependent launch between the 2T dependent launches of an evaluation: the next kernel's CTAs are
   // scheduled, and run their prologue up to griddepcontrol.wait, while the previous kernel drains.  Measured on B200
   // (ms per gradient, T = 10, without / with): fp32 N = 4500 0.647 / 0.625, 6000 0.965 / 0.947, 8000 1.509 / 1.506,
-  // 20 000 7.93 / 7.95; fp64 N = 3000 0.735 / 0.715, 5000 1.620 / 1.602, 10 000 5.708 / 5.693.  On for single
-  // unpartitioned problems below 8000 landmarks (LMS_PDL=0/1 overrides).
-  pdl_ = batch == 1 && c.n < 8000;
+  // 20 000 7.93 / 7.95; fp64 N = 3000 0.735 / 0.715, 5000 1.620 / 1.602, 10 000 5.708 / 5.693 -- but a LOSS around
+  // N = 1500-2000, where the tiled path is not the default anyway (fp32 2000: 0.244 / 0.285, fp64 2000: 0.429 / 0.637).
+  // On for single unpartitioned problems of 2400 to 8000 landmarks (LMS_PDL=0/1 overrides).
+  pdl_ = batch == 1 && c.n >= 2400 && c.n < 8000;
   if (const char* e = std::getenv("LMS_PDL")) pdl_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("LMS_CLUSTER")) cluster_combine_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("LMS_SMALL")) small_enabled_ = std::atoi(e) != 0;
