@@ -6,7 +6,9 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 namespace lms {
@@ -35,16 +37,25 @@ void dev_free(T*& p)
 }  // namespace
 
 // ---- construction ------------------------------------------------------------------------------------
+#ifdef LMS_TIME_CTOR  // measurement builds: where the handle's construction time goes
+inline std::chrono::steady_clock::time_point& ctor_prev() { static std::chrono::steady_clock::time_point t; return t; }
+#define LMS_CTOR_T(i) do { auto t_now = std::chrono::steady_clock::now(); if ((i) == 0) ctor_prev() = t_now; std::fprintf(stderr, "ctor %d: +%.3f ms\n", (i), std::chrono::duration<double, std::milli>(t_now - ctor_prev()).count()); ctor_prev() = t_now; } while (0)
+#else
+#define LMS_CTOR_T(i) do {} while (0)
+#endif
 template <typename T, int D>
 System<T, D>::System(const lms_config& c, int batch_count)
 {
   cfg = c;
   batch = std::max(batch_count, 1);
+  LMS_CTOR_T(0);
   LMS_CUDA(cudaSetDevice(c.device));
-  cudaDeviceProp prop;
-  LMS_CUDA(cudaGetDeviceProperties(&prop, c.device));
-  if (prop.major != 10) throw StatusError{LMS_ERR_CUDA, "device is not sm_100 (B200); no fallback path exists"};
-  num_sms_ = prop.multiProcessorCount;
+  // (two attribute queries instead of cudaGetDeviceProperties: that call alone took 2.4 ms of a 5.6 ms construction)
+  int cc_major = 0;
+  LMS_CUDA(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, c.device));
+  if (cc_major != 10) throw StatusError{LMS_ERR_CUDA, "device is not sm_100 (B200); no fallback path exists"};
+  LMS_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, c.device));
+  LMS_CTOR_T(1);
   // Programmatic dependent launch between the 2T dependent launches of an evaluation: the next kernel's CTAs are
   // scheduled, and run their prologue up to griddepcontrol.wait, while the previous kernel drains.  Measured on B200
   // (ms per gradient, T = 10, without / with): fp32 N = 4500 0.647 / 0.625, 6000 0.965 / 0.947, 8000 1.509 / 1.506,
@@ -61,6 +72,7 @@ System<T, D>::System(const lms_config& c, int batch_count)
   LMS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   LMS_CUDA(cudaEventCreate(&ev_begin_));
   LMS_CUDA(cudaEventCreate(&ev_end_));
+  LMS_CTOR_T(2);
 
   // Constants rounded as the reference rounds them (shooting.hpp:63-68,114-115).
   inv_sig2_ = T(1) / (T(c.sigma) * T(c.sigma));
@@ -75,6 +87,7 @@ System<T, D>::System(const lms_config& c, int batch_count)
   // 197.6 ms per gradient, same session), but twice the row-tile size, which mid-size and batched problems pay
   // for in parallelism.  Variant 11 pins the two-row shapes for A/B.
   pick_kernels(/*partitioned=*/false);
+  LMS_CTOR_T(3);
 
   max_t_ = std::max(c.max_timesteps, 1);
   const long long N = (long long)c.n;
@@ -96,12 +109,22 @@ System<T, D>::System(const lms_config& c, int batch_count)
   d_io_ = dev_alloc_zero<double>(4 * io_cap_);
   d_x_ = dev_alloc_zero<double>(std::max((size_t)stride_ * D, B * (size_t)N * D));
   d_ids_ = dev_alloc_zero<int>(B);
-  LMS_CUDA(cudaMallocHost(&h_scalars_, 4 * B * sizeof(double)));
+  LMS_CTOR_T(4);
+  // one pinned (mapped) allocation: the scalar records of every problem, and -- single problems -- x | grad | scalars
+  // for the persistent kernel's zero-copy host-buffer calls (a pinned allocation costs 1-2.5 ms: one, not two)
+  {
+    const size_t zc = (B == 1 && small_enabled_ && N <= (long long)small_max_n_) ? 2 * (size_t)N * D + 4 : 0;
+    LMS_CUDA(cudaHostAlloc(&h_scalars_, (4 * B + zc) * sizeof(double), cudaHostAllocMapped));
+    h_zc_ = zc ? h_scalars_ + 4 * B : nullptr;
+  }
+  LMS_CTOR_T(5);
   part_tiles_ = (int)(stride_ / kThreads);
   warp_part_ = dev_alloc_zero<double>((size_t)2 * num_sms_ * kSmallMaxWarps);
   small_bar_ = dev_alloc_zero<unsigned>(64);
   alloc_exchange_arena();
+  LMS_CTOR_T(6);
   alloc_partials();
+  LMS_CTOR_T(7);
 }
 
 // Variant 0 picks the shapes by problem size.  From N = 16 000 on (fp32) four rows per thread pay (variant 25;
@@ -191,8 +214,7 @@ System<T, D>::~System()
   dev_free(d_io_);
   dev_free(d_x_);
   dev_free(d_ids_);
-  if (h_scalars_) cudaFreeHost(h_scalars_);
-  if (h_zc_) cudaFreeHost(h_zc_);
+  if (h_scalars_) cudaFreeHost(h_scalars_);  // h_zc_ lives in the same allocation
   for (auto e : events_) cudaEventDestroy(e);
   if (ev_begin_) cudaEventDestroy(ev_begin_);
   if (ev_end_) cudaEventDestroy(ev_end_);
@@ -511,7 +533,6 @@ void System<T, D>::plan_small()
       break;
     }
   }
-  if (!h_zc_) LMS_CUDA(cudaHostAlloc(&h_zc_, (2 * (size_t)cfg.n * D + 4) * sizeof(double), cudaHostAllocMapped));
   if (small_cluster_ > 1) {
     // cluster launches are whole clusters (CTAs without rows still fetch their share and take part in the barriers)
     const int g = std::min(small_grid_cap_, (int)round_up(grid, small_cluster_));
