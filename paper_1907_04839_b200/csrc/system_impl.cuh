@@ -508,8 +508,14 @@ void System<T, D>::plan_small()
     return e ? std::atoi(e) : 0;
   }();
   small_cluster_ = 1;
+  // Measured on B200 (ms per gradient, T = 10, clusters of 8 / 4 / 2 / none): fp32 N = 1000 0.103 / 0.097 / 0.099 / 0.101,
+  // 2000 0.194 / 0.182 / 0.176 / 0.180, 4000 0.465 / 0.485 / 0.456 / 0.465; fp64 N = 2000 0.387 / 0.396 / 0.379 / 0.388: a
+  // shared fetch also couples the CTAs of a cluster (a chunk's barrier completes when the slowest of them has
+  // issued its pieces), so small clusters win once the sweeps dominate.
+  // (N = 1500: fp32 0.133 with clusters of 4 against 0.138 with 2; fp64 0.264 against 0.258)
+  const int prefer = n() <= (sizeof(T) == 4 ? 1700 : 1200) ? 4 : 2;
   for (int cs : {8, 4, 2}) {
-    if (force_cs > 0 && cs != force_cs) continue;
+    if (force_cs > 0 ? cs != force_cs : cs > prefer) continue;
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(num_sms_ / cs * cs);
     lc.blockDim = dim3(small_threads_);
