@@ -61,8 +61,12 @@ constexpr int kSmallMaxN64 = 2048;
 
 template <typename T>
 struct SmallShape {
-  static constexpr int kChunk = sizeof(T) == 4 ? 512 : 256;  // columns per staged chunk
-  static constexpr int kMaxChunks = 8;                        // chunk buffers (all resident during a step)
+#ifndef LMS_SMALL_CHUNKS
+#define LMS_SMALL_CHUNKS 2  // measured on B200 (ms per gradient, 16 / 8 / 4 / 2 / 1 chunks): fp32 N = 2000 0.206 / 0.179 / 0.163 /
+                            // 0.162 / 0.161, N = 4000 0.520 / 0.462 / 0.427 / 0.411 / 0.415; fp64 N = 2000 0.447 / 0.384 / 0.347 / 0.332 / 0.334
+#endif
+  static constexpr int kMaxChunks = LMS_SMALL_CHUNKS;                              // chunk buffers (all resident during a step)
+  static constexpr int kChunk = (sizeof(T) == 4 ? 4096 : 2048) / kMaxChunks;       // columns per staged chunk
   static constexpr int kCols = kChunk * kMaxChunks;           // shared-memory array length per component
   static constexpr int kRowsPerSlot = sizeof(T) == 4 ? 2 : 1;
 };
@@ -326,14 +330,17 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
     asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(cl_size));
 #pragma unroll 1
     for (int c = 0; c < a.n_chunks; ++c) {
-      if (lane == 0) mbar_expect_tx(&bars[c], (unsigned)(NC * CH * sizeof(T)));
+      // the last chunk ends with the plane (planes are padded to 512 columns, chunks may be longer)
+      const long long left = a.stride - (long long)c * CH;
+      const unsigned cols = (unsigned)(left < CH ? left : CH);
+      if (lane == 0) mbar_expect_tx(&bars[c], (unsigned)(NC * cols * sizeof(T)));
       if (lane < NC) {
         T* dst = tile + (long long)lane * NTOT + (long long)c * CH;
         const T* src = plane(lane) + (long long)c * CH;
         if (cl_size == 1)
-          bulk_g2s(dst, src, (unsigned)(CH * sizeof(T)), &bars[c]);
+          bulk_g2s(dst, src, (unsigned)(cols * sizeof(T)), &bars[c]);
         else if ((unsigned)(c * NC + lane) % cl_size == cl_rank)
-          bulk_g2s_multicast(dst, src, (unsigned)(CH * sizeof(T)), &bars[c], (unsigned short)((1u << cl_size) - 1u));
+          bulk_g2s_multicast(dst, src, (unsigned)(cols * sizeof(T)), &bars[c], (unsigned short)((1u << cl_size) - 1u));
       }
     }
   } else {

@@ -477,7 +477,7 @@ void System<T, D>::plan_small()
   use_small_ = false;
   if (!small_enabled_ || batch != 1 || comm_active_ || n() <= 0 || n() > small_max_n_) return;
   constexpr int CH = SmallShape<T>::kChunk;
-  if (stride_ % CH != 0 || ceil_div(n(), CH) > SmallShape<T>::kMaxChunks) return;  // every chunk gets its own buffer
+  if (ceil_div(n(), CH) > SmallShape<T>::kMaxChunks) return;  // the whole state is staged at once
   // rows per slot: one packed row pair in fp32, one row in fp64.  (Two packed pairs per slot -- every column load
   // serving both, as in the tiled R = 4 kernels; the kernel template takes RS = 4 -- measured slower on the B200:
   // N = 4000 0.504 vs 0.490 ms, N = 2000 0.188 vs 0.185 ms; it spills at the 128-register cap of a 512-thread CTA.)
@@ -508,12 +508,13 @@ void System<T, D>::plan_small()
     return e ? std::atoi(e) : 0;
   }();
   small_cluster_ = 1;
-  // Measured on B200 (ms per gradient, T = 10, clusters of 8 / 4 / 2 / none): fp32 N = 1000 0.103 / 0.097 / 0.099 / 0.101,
-  // 2000 0.194 / 0.182 / 0.176 / 0.180, 4000 0.465 / 0.485 / 0.456 / 0.465; fp64 N = 2000 0.387 / 0.396 / 0.379 / 0.388: a
-  // shared fetch also couples the CTAs of a cluster (a chunk's barrier completes when the slowest of them has
-  // issued its pieces), so small clusters win once the sweeps dominate.
-  // (N = 1500: fp32 0.133 with clusters of 4 against 0.138 with 2; fp64 0.264 against 0.258)
-  const int prefer = n() <= (sizeof(T) == 4 ? 1700 : 1200) ? 4 : 2;
+  // Measured on B200 with the state staged in two chunks (ms per gradient, T = 10, clusters of 8 / 4 / 2 / none): fp32
+  // N = 500 0.081 / 0.077 / 0.079 / 0.078, 1000 0.101 / 0.093 / 0.096 / 0.094, 2000 0.179 / 0.166 / 0.162 / 0.158, 4000
+  // 0.409 / 0.446 / 0.411 / 0.409; fp64 N = 1000 0.156 / 0.144 / 0.145 / 0.141, 2000 0.331 / 0.355 / 0.332 / 0.331.  A shared
+  // fetch also couples the CTAs of a cluster (a chunk's barrier completes when the slowest of them has issued its
+  // pieces), and with few, large copies L2 serves 148 CTAs as fast as 37 clusters: clusters of four only for the
+  // smallest problems, none above.
+  const int prefer = n() <= (sizeof(T) == 4 ? 1700 : 700) ? 4 : 1;
   for (int cs : {8, 4, 2}) {
     if (force_cs > 0 ? cs != force_cs : cs > prefer) continue;
     cudaLaunchConfig_t lc{};
