@@ -12,13 +12,16 @@
 //   rows      "slots" of RS rows (fp32: the 2 rows of a packed FFMA2 operand; fp64: 1 row) are dealt to the CTAs
 //             in contiguous, equal (+-1) runs.  Row operands are warp-uniform registers.
 //   columns   every CTA pulls the whole landmark state into shared memory, one contiguous array per component,
-//             in chunks of 512 (fp64: 256) columns with bulk-async copies (cp.async.bulk + one mbarrier per chunk:
+//             in chunks of 2048 (fp64: 1024) columns with bulk-async copies (cp.async.bulk + one mbarrier per chunk:
 //             reads L2, so the state other CTAs wrote before the barrier is seen without any L1 concern).  All
-//             chunks of a step are in flight at once (up to 8: N <= 4096 fp32 / 2048 fp64) and a warp waits only
-//             for the chunks it is about to read, so there is no CTA-wide synchronisation inside a sweep.
+//             chunks of a window are in flight at once and a warp waits only for the chunks it is about to read,
+//             so there is no CTA-wide synchronisation inside a window.  A window is what fits 192 KB: 8192 columns
+//             (fp64: 4096) of the forward sweep's 2D components, half as many of the adjoint's 4D; wider problems
+//             sweep two adjoint windows per step, their pieces parked separately and added in column order.
 //   work      a CTA with s slots has s x G work items (slot, group of 32 columns), slot-major; its 16 warps take
 //             equal contiguous runs of that list (stream-K inside the CTA), so every warp is busy for the same
-//             time whatever s is.  A run touches at most two slots: two "pieces" (slot, group range) per warp.
+//             time whatever s is.  A run touches at most three slots: up to three "pieces" (slot, group range) per
+//             warp and window.
 //             Inside a piece lane l takes U consecutive columns of each block of 32 U (one LDS.128 / LDS.64 per
 //             component serves U pairs per row: U independent dependency chains in one basic block).
 //   sums      per lane ascending columns; a fixed transposing shuffle tree over the lanes of the piece; the
@@ -36,11 +39,17 @@ namespace lms {
 
 constexpr int kSmallWarps = 16;     // warps per CTA
 constexpr int kSmallMaxWarps = kSmallWarps;
-constexpr int kSmallMaxSlots = 16;  // slots per CTA (a warp's run of work then spans at most two slots)
-// Largest n the persistent kernel is chosen for (LMS_SMALL_MAX_N overrides): the shared-memory capacity for the
-// staged state (8 chunks), see SmallShape.
-constexpr int kSmallMaxN32 = 4096;
-constexpr int kSmallMaxN64 = 2048;
+constexpr int kSmallMaxSlots = 32;  // slots per CTA (a warp's run of work then spans at most three slots)
+constexpr int kSmallMaxPieces = 3;  // ... pieces per warp and window
+constexpr int kSmallMaxWindows = 2; // adjoint windows (the forward sweep has one)
+// Largest n the persistent kernel is chosen for (LMS_SMALL_MAX_N overrides): fp32 the capacity (measured on B200,
+// persistent / tiled ms per gradient: N = 5000 0.635 / 0.704, 6000 0.879 / 0.941, 7000 1.129 / 1.192, 8192 1.490 / 1.509);
+// fp64 the crossover with the tiled path (N = 2049 0.380 / 0.507, 3000 0.685 / 0.715, 4096 1.144 / 1.110).
+constexpr int kSmallMaxN32 = 8192;
+constexpr int kSmallMaxN64 = 3400;
+// hard limit: one forward window = two adjoint windows (SmallShape)
+constexpr int kSmallCapacity32 = 8192;
+constexpr int kSmallCapacity64 = 4096;
 
 // LMS_SMALL_TRACE: phase timestamps (globaltimer, ns) of CTA 0 into SmallArgs::trace -- a measurement build only
 // (scripts/small_trace.py); the shipped library compiles the macro to nothing.
@@ -61,13 +70,17 @@ constexpr int kSmallMaxN64 = 2048;
 
 template <typename T>
 struct SmallShape {
+  // The staged state: 192 KB of shared memory hold every component of 4096 (fp64: 2048) columns in the adjoint sweep
+  // (4D components) and of twice as many in the forward sweep (2D components).  A sweep stages one such WINDOW at a
+  // time, in chunks with one mbarrier each; problems wider than a window sweep several, one after the other.
 #ifndef LMS_SMALL_CHUNKS
-#define LMS_SMALL_CHUNKS 2  // measured on B200 (ms per gradient, 16 / 8 / 4 / 2 / 1 chunks): fp32 N = 2000 0.206 / 0.179 / 0.163 /
-                            // 0.162 / 0.161, N = 4000 0.520 / 0.462 / 0.427 / 0.411 / 0.415; fp64 N = 2000 0.447 / 0.384 / 0.347 / 0.332 / 0.334
+#define LMS_SMALL_CHUNKS 2  // chunks per adjoint window.  Measured on B200 (ms per gradient, 16 / 8 / 4 / 2 / 1 chunks): fp32 N = 2000 0.206 /
+                            // 0.179 / 0.163 / 0.162 / 0.161, N = 4000 0.520 / 0.462 / 0.427 / 0.411 / 0.415; fp64 N = 2000 0.447 / 0.384 / 0.347 / 0.332 / 0.334
 #endif
-  static constexpr int kMaxChunks = LMS_SMALL_CHUNKS;                              // chunk buffers (all resident during a step)
-  static constexpr int kChunk = (sizeof(T) == 4 ? 4096 : 2048) / kMaxChunks;       // columns per staged chunk
-  static constexpr int kCols = kChunk * kMaxChunks;           // shared-memory array length per component
+  static constexpr int kCols = sizeof(T) == 4 ? 4096 : 2048;   // columns per component in an adjoint window
+  static constexpr int kColsFwd = 2 * kCols;                   // ... in a forward window
+  static constexpr int kChunk = kCols / LMS_SMALL_CHUNKS;      // columns per staged chunk
+  static constexpr int kMaxChunks = kColsFwd / kChunk;         // chunk barriers
   static constexpr int kRowsPerSlot = sizeof(T) == 4 ? 2 : 1;
 };
 
@@ -239,62 +252,76 @@ __device__ __forceinline__ void load_cols(const T* p, T (&v)[U])
 // What a thread needs to know about the CTA's work list; the same for every time step, so it is worked out once
 // per launch (the per-step code between two sweeps is latency-critical and mostly cold in the instruction cache:
 // it is kept as short as possible).
-struct SmallPlan {
-  int slot0, s_b;       // the CTA's slots [slot0, slot0 + s_b)
-  int n_pieces;         // pieces of this warp's run (0..2)
-  int sl[2], g0[2], g1[2];  // slot (CTA-local) and 32-column groups [g0, g1) of each
-  int pid0;             // index of the warp's first piece among the CTA's pieces (ascending work-list order)
-  int epi_first, epi_count;  // epilogue thread: its slot's pieces are [epi_first, epi_first + epi_count)
+struct SmallWarpPlan {  // a warp's run of one window's work list: up to three pieces (slot, groups [g0, g1))
+  int n_pieces;
+  int pid0;  // index of the warp's first piece among the CTA's pieces of that window (ascending work-list order)
+  int sl[kSmallMaxPieces], g0[kSmallMaxPieces], g1[kSmallMaxPieces];
+};
+struct SmallEpiPlan {  // epilogue thread: its slot's pieces of that window are [first, first + count)
+  int first, count;
 };
 
+// The work list of one window (s_b slots x Gw groups, slot-major) cut into sixteen equal contiguous runs.  Every
+// thread walks the sixteen runs: lane 0 of a warp records the warp's run, epilogue thread t (component t % D of the
+// CTA's row t / D) where its slot's pieces lie.
 template <int RS, int D>
-__device__ __forceinline__ SmallPlan small_plan(int n)
+__device__ __forceinline__ void small_plan_window(int s_b, int Gw, SmallWarpPlan* wplan, SmallEpiPlan* eplan)
 {
-  SmallPlan p;
-  // (the lane-0 shuffle tells ptxas the warp index -- and every count derived from it -- is warp-uniform)
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-  const int slots = (n + RS - 1) / RS;
-  p.slot0 = (int)((long long)blockIdx.x * slots / gridDim.x);
-  p.s_b = (int)((long long)(blockIdx.x + 1) * slots / gridDim.x) - p.slot0;
-  const int G = (n + 31) / 32;  // live groups
-  const int total = p.s_b * G;
-  p.n_pieces = 0;
-  p.pid0 = 0;
-  p.sl[0] = p.sl[1] = p.g0[0] = p.g0[1] = p.g1[0] = p.g1[1] = 0;
-  // epilogue thread t finishes (row t / D of the CTA, component t % D)
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+  const int total = s_b * Gw;
   const int my_slot = (int)threadIdx.x / (RS * D);
-  p.epi_first = 0;
-  p.epi_count = 0;
-  int pid = 0;
+  SmallWarpPlan mine;
+  mine.n_pieces = 0;
+  mine.pid0 = 0;
+#pragma unroll
+  for (int j = 0; j < kSmallMaxPieces; ++j) mine.sl[j] = mine.g0[j] = mine.g1[j] = 0;
+  int first = 0, count = 0, pid = 0;
   for (int w = 0; w < kSmallWarps; ++w) {
     const int r0 = w * total / kSmallWarps, r1 = (w + 1) * total / kSmallWarps;
     if (r1 == r0) continue;  // fewer items than warps
-    const int s0 = r0 / G, s1 = (r1 - 1) / G;  // s1 <= s0 + 1: a run is at most G items long
+    const int s0 = r0 / Gw, s1 = (r1 - 1) / Gw;  // s1 <= s0 + 2: a run is at most 2 Gw items long
     if (w == warp) {
-      p.n_pieces = s1 - s0 + 1;
-      p.pid0 = pid;
-      p.sl[0] = s0;
-      p.g0[0] = r0 - s0 * G;
-      p.g1[0] = s1 > s0 ? G : r1 - s0 * G;
-      p.sl[1] = s1;
-      p.g0[1] = 0;
-      p.g1[1] = r1 - s1 * G;
+      mine.n_pieces = s1 - s0 + 1;
+      mine.pid0 = pid;
+#pragma unroll
+      for (int j = 0; j < kSmallMaxPieces; ++j) {
+        const int sl = s0 + j;
+        if (sl <= s1) {
+          mine.sl[j] = sl;
+          mine.g0[j] = j == 0 ? r0 - s0 * Gw : 0;
+          mine.g1[j] = sl == s1 ? r1 - s1 * Gw : Gw;
+        }
+      }
     }
     for (int sl = s0; sl <= s1; ++sl) {
-      if (sl < my_slot) ++p.epi_first;
-      if (sl == my_slot) ++p.epi_count;
+      if (sl < my_slot) ++first;
+      if (sl == my_slot) ++count;
     }
     pid += s1 - s0 + 1;
   }
-  return p;
+  if (lane == 0) wplan[warp] = mine;
+  if ((int)threadIdx.x < kSmallMaxSlots * RS * D) {
+    eplan[threadIdx.x].first = first;
+    eplan[threadIdx.x].count = count;
+  }
 }
+
+// What a step needs to know about the CTA's share of the problem; worked out once per launch (the per-step code
+// between two sweeps is latency-critical and mostly cold in the instruction cache: it is kept as short as possible).
+struct SmallCtx {
+  int slot0, s_b;                      // the CTA's slots [slot0, slot0 + s_b)
+  int adj_windows;                     // windows of the adjoint sweep (1 or 2); the forward sweep has one
+  const SmallWarpPlan* wplan;          // [1 + kSmallMaxWindows][kSmallWarps]: forward, adjoint window 0, adjoint window 1
+  const SmallEpiPlan* eplan;           // [1 + kSmallMaxWindows][epilogue threads]
+  int epi_stride;                      // epilogue threads per plan
+};
 
 // One time step for this CTA's rows.  MODE kFwd: state -> out = next snapshot (Euler, shooting.hpp:205-211) with
 // the first / last step extras; MODE kAdj: (state, adj_in) -> out = next adjoint state (:302-306).
 template <typename T, int D, int MODE, int RS>
-__device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPlan& pl, const T* __restrict__ state,
+__device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallCtx& cx, const T* __restrict__ state,
                                            const T* __restrict__ adj_in, T* __restrict__ out, unsigned epi, int step_no,
-                                           T* tile, T* part, T* rowbuf, unsigned long long* bars, unsigned& phase,
+                                           T* tile, T* part, T* rowbuf, unsigned long long* bars, unsigned& phase_bits,
                                            double& hsum, double& msum, const double* exp_tbl, int trace_base)
 {
   LMS_TRACE_POINT(a, trace_base + 0);
@@ -302,12 +329,18 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
   constexpr int NC = S::kColComps, NR = S::kRowComps, NA = S::kAcc;
   constexpr bool F32 = sizeof(T) == 4;
   constexpr int CH = SmallShape<T>::kChunk;
-  constexpr int NTOT = SmallShape<T>::kCols;
-  constexpr int GPC = CH / 32;  // 32-column groups per chunk
-  constexpr int NV = RS * NA;   // sums per slot
-  constexpr int NRMAX = 4 * D;  // row operands per row in the adjoint sweep (rowbuf is sized for it)
+  constexpr int NTOT = MODE == kAdj ? SmallShape<T>::kCols : SmallShape<T>::kColsFwd;  // columns per window
+  constexpr int WCH = NTOT / CH;  // chunks per window
+  constexpr int GPC = CH / 32;    // 32-column groups per chunk
+  constexpr int GPW = NTOT / 32;  // ... per window
+  constexpr int NV = RS * NA;     // sums per slot
+  constexpr int NRMAX = 4 * D;    // row operands per row in the adjoint sweep (rowbuf is sized for it)
+  constexpr int PMAX = kSmallWarps * kSmallMaxPieces;  // pieces per window
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  const int n_windows = MODE == kAdj ? cx.adj_windows : 1;
+  const int plan0 = MODE == kAdj ? 1 : 0;
+  const int G = (a.n + 31) / 32;  // live groups
 
   auto plane = [&](int k) -> const T* {
     if constexpr (MODE == kAdj)
@@ -315,192 +348,208 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallPla
     else
       return state + (long long)k * a.stride;
   };
-  // Every chunk of this step's state is fetched at once: one bulk copy per (chunk, component plane), issued by
-  // lanes 0..NC-1 of the last warp side by side; lane 0's arrive.expect_tx is a chunk barrier's one arrival, so its
-  // phase cannot complete before every byte has been expected and delivered.  (All warps passed the grid
-  // barrier's __syncthreads since they last read these buffers.)
-  // All 148 CTAs pull the same bytes at the same moment, and the L2 -> SM fabric (not latency) is what the first
-  // chunk then waits for (measured: 96 KB per CTA take 3 us at N = 2000).  Launched as thread-block clusters, the
-  // CTAs of a cluster share the fetch: piece (chunk, plane) is requested by ONE of them and multicast into the
-  // same buffer offset of all (and completes on the same mbarrier offset of all), so L2 serves 1/cluster-size of
-  // the traffic.
-  if (warp == kSmallWarps - 1) {
-    unsigned cl_rank, cl_size;
-    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(cl_rank));
-    asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(cl_size));
-#pragma unroll 1
-    for (int c = 0; c < a.n_chunks; ++c) {
-      // the last chunk ends with the plane (planes are padded to 512 columns, chunks may be longer)
-      const long long left = a.stride - (long long)c * CH;
-      const unsigned cols = (unsigned)(left < CH ? left : CH);
-      if (lane == 0) mbar_expect_tx(&bars[c], (unsigned)(NC * cols * sizeof(T)));
-      if (lane < NC) {
-        T* dst = tile + (long long)lane * NTOT + (long long)c * CH;
-        const T* src = plane(lane) + (long long)c * CH;
-        if (cl_size == 1)
-          bulk_g2s(dst, src, (unsigned)(cols * sizeof(T)), &bars[c]);
-        else if ((unsigned)(c * NC + lane) % cl_size == cl_rank)
-          bulk_g2s_multicast(dst, src, (unsigned)(cols * sizeof(T)), &bars[c], (unsigned short)((1u << cl_size) - 1u));
-      }
-    }
-  } else {
-    // ---- row operands of the CTA's rows: one value per thread (of the other warps), read past L1 (other CTAs wrote
-    // them before the grid barrier) and parked in shared memory for the sweeps and the epilogue; the fetch
-    // overlaps the chunk copies.  kSmallMaxSlots * RS * NR <= 384 values <= 15 warps ----
-    for (int t = threadIdx.x; t < pl.s_b * RS * NR; t += 32 * (kSmallWarps - 1)) {
-      const int rl = t / NR, k = t - rl * NR;  // row of the CTA, component
-      const long long row = (long long)pl.slot0 * RS + rl;
-      // [slot][component][row of the slot]: a slot's packed (row 0, row 1) operand is one 8-byte word
-      rowbuf[((rl / RS) * NRMAX + k) * RS + (rl % RS)] = row < a.n ? __ldcg(plane(k) + row) : T(0);
-    }
-  }
-  __syncthreads();
-  LMS_TRACE_POINT(a, trace_base + 1);
   const unsigned bars_u32 = smem_u32(bars);
 
-  // ---- the warp's pieces: (slot, groups [g0, g1)) ----
-  constexpr int U = F32 ? (MODE == kAdj ? (RS == 4 ? 1 : LMS_SMALL_UA) : (RS == 4 ? 2 : LMS_SMALL_UF))
-                        : (MODE == kAdj ? LMS_SMALL_UA64 : LMS_SMALL_UF64);
-  int waited = 0;  // chunks [0, waited) have landed
-  // A run that wraps from the tail of one slot into the head of the next is swept head first: the head starts at
-  // column 0, whose chunk lands first, while the tail's chunks are the last to arrive (a warp waits only for the
-  // chunks it reads).  The epilogue adds a slot's pieces in ascending column order whatever order they were swept in.
 #pragma unroll 1
-  for (int pc = pl.n_pieces - 1; pc >= 0; --pc) {
-    const int sl = pc ? pl.sl[1] : pl.sl[0];
-    const int g0 = pc ? pl.g0[1] : pl.g0[0];
-    const int g1 = pc ? pl.g1[1] : pl.g1[0];
-    T rv[RS][NR];  // warp-uniform
-    if constexpr (RS > 1) {
-#pragma unroll
-      for (int k = 0; k < NR; ++k) {
-        T v[RS];
-        load_cols<T, RS>(rowbuf + (sl * NRMAX + k) * RS, v);
-#pragma unroll
-        for (int h = 0; h < RS; ++h) rv[h][k] = v[h];
+  for (int win = 0; win < n_windows; ++win) {
+    // everyone is done reading the previous window (the first window of a step: the grid barrier's __syncthreads)
+    if (win > 0) __syncthreads();
+    // Every chunk of the window is fetched at once: one bulk copy per (chunk, component plane), issued by lanes
+    // 0..NC-1 of the last warp side by side; lane 0's arrive.expect_tx is a chunk barrier's one arrival, so its phase
+    // cannot complete before every byte has been expected and delivered.  Launched as thread-block clusters, the CTAs
+    // of a cluster share the fetch: piece (chunk, plane) is requested by ONE of them and multicast into the same
+    // buffer offset of all (and completes on the same mbarrier offset of all).
+    const int chunk0 = win * WCH;
+    const int n_ch = a.n_chunks - chunk0 < WCH ? a.n_chunks - chunk0 : WCH;
+    if (warp == kSmallWarps - 1) {
+      unsigned cl_rank, cl_size;
+      asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(cl_rank));
+      asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(cl_size));
+#pragma unroll 1
+      for (int c = 0; c < n_ch; ++c) {
+        // the last chunk ends with the plane (planes are padded to 512 columns, chunks may be longer)
+        const long long col = (long long)(chunk0 + c) * CH;
+        const long long left = a.stride - col;
+        const unsigned cols = (unsigned)(left < CH ? left : CH);
+        if (lane == 0) mbar_expect_tx(&bars[c], (unsigned)(NC * cols * sizeof(T)));
+        if (lane < NC) {
+          T* dst = tile + (long long)lane * NTOT + (long long)c * CH;
+          const T* src = plane(lane) + col;
+          if (cl_size == 1)
+            bulk_g2s(dst, src, (unsigned)(cols * sizeof(T)), &bars[c]);
+          else if ((unsigned)(c * NC + lane) % cl_size == cl_rank)
+            bulk_g2s_multicast(dst, src, (unsigned)(cols * sizeof(T)), &bars[c], (unsigned short)((1u << cl_size) - 1u));
+        }
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < NR; ++k) rv[0][k] = rowbuf[sl * NRMAX + k];
+    } else if (win == 0) {
+      // ---- row operands of the CTA's rows: one value per thread (of the other warps), read past L1 (other CTAs
+      // wrote them before the grid barrier) and parked in shared memory for the sweeps and the epilogue; the fetch
+      // overlaps the chunk copies ----
+      for (int t = threadIdx.x; t < cx.s_b * RS * NR; t += 32 * (kSmallWarps - 1)) {
+        const int rl = t / NR, k = t - rl * NR;  // row of the CTA, component
+        const long long row = (long long)cx.slot0 * RS + rl;
+        // [slot][component][row of the slot]: a slot's packed (row 0, row 1) operand is one 8-byte word
+        rowbuf[((rl / RS) * NRMAX + k) * RS + (rl % RS)] = row < a.n ? __ldcg(plane(k) + row) : T(0);
+      }
+    }
+    if (win == 0) {
+      __syncthreads();
+      LMS_TRACE_POINT(a, trace_base + 1);
     }
 
-    constexpr int RPK = F32 ? RS / 2 : 1;  // packed row pairs per slot (fp32)
-    T acc[NV];
-    float2 ri2[RPK][NR], acc2[RPK][NA];
-    float2 kexp2, ns2, neg1;
-    if constexpr (F32) {
-#pragma unroll
-      for (int rp = 0; rp < RPK; ++rp) {
+    // ---- the warp's pieces of this window: (slot, groups [g0, g1)), groups counted from the window's first ----
+    const SmallWarpPlan wp = cx.wplan[(plan0 + win) * kSmallWarps + warp];
+    constexpr int U = F32 ? (MODE == kAdj ? (RS == 4 ? 1 : LMS_SMALL_UA) : (RS == 4 ? 2 : LMS_SMALL_UF))
+                          : (MODE == kAdj ? LMS_SMALL_UA64 : LMS_SMALL_UF64);
+    int waited = 0;  // chunks [0, waited) of this window have landed
+    // A run that wraps from the tail of one slot into the head of the next is swept head first: the head starts at
+    // the window's first column, whose chunk lands first, while the tail's chunks are the last to arrive (a warp
+    // waits only for the chunks it reads).  The epilogue adds a slot's pieces in ascending column order whatever
+    // order they were swept in.
+#pragma unroll 1
+    for (int pc = wp.n_pieces - 1; pc >= 0; --pc) {
+      const int sl = pc == 0 ? wp.sl[0] : (pc == 1 ? wp.sl[1] : wp.sl[2]);
+      const int g0 = pc == 0 ? wp.g0[0] : (pc == 1 ? wp.g0[1] : wp.g0[2]);
+      const int g1 = pc == 0 ? wp.g1[0] : (pc == 1 ? wp.g1[1] : wp.g1[2]);
+      T rv[RS][NR];  // warp-uniform
+      if constexpr (RS > 1) {
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
-          const float lo = (float)rv[2 * rp][k], hi = (float)rv[2 * rp + 1][k];
-          ri2[rp][k] = k < D ? make_float2(-lo, -hi) : make_float2(lo, hi);  // pair_term_packed takes -q_i
+          T v[RS];
+          load_cols<T, RS>(rowbuf + (sl * NRMAX + k) * RS, v);
+#pragma unroll
+          for (int h = 0; h < RS; ++h) rv[h][k] = v[h];
         }
-#pragma unroll
-        for (int k = 0; k < NA; ++k) acc2[rp][k] = make_float2(0.f, 0.f);
-      }
-      kexp2 = splat2((float)a.kexp);
-      ns2 = splat2(-(float)a.inv_sig2);
-      neg1 = splat2(-1.f);
-    } else {
-#pragma unroll
-      for (int k = 0; k < NV; ++k) acc[k] = T(0);
-    }
-    auto evaluate = [&](const T(&cj)[NC]) {
-      if constexpr (F32) {
-        float2 cj2[NC];
-#pragma unroll
-        for (int k = 0; k < NC; ++k) cj2[k] = splat2((float)cj[k]);
-#pragma unroll
-        for (int rp = 0; rp < RPK; ++rp) pair_term_packed<D, MODE>(ri2[rp], cj2, acc2[rp], kexp2, ns2, neg1);
       } else {
-        pair_term<T, D, MODE>(rv[0], cj, acc, a.kexp, a.inv_sig2, exp_tbl);
-      }
-    };
-    // The piece chunk by chunk: a chunk is waited for once (they land roughly in order, so everything up to it is
-    // waited for), then its groups are swept without further checks -- blocks of U groups (lane l takes the U
-    // consecutive columns 32 U b + U l ..: one vector load per component), then single groups up to the chunk's
-    // end.  Chunks start at multiples of 16 groups, so only a piece's first chunk can have such a remainder.
-    // Counters and offsets are warp-uniform (uniform datapath: no vector-register reads in the loop control).
-    const T* lane_blk = tile + lane * U;
-    const T* lane_one = tile + lane;
-    int g = g0;
-#pragma unroll 1
-    while (g < g1) {
-      const int c = (int)((unsigned)g / (unsigned)GPC);
-      if (c >= waited) {
-#pragma unroll 1
-        do {
-          mbar_wait_u32(bars_u32 + 8u * (unsigned)waited, phase);
-          ++waited;
-        } while (waited <= c);
-      }
-      const int gend = (c + 1) * GPC < g1 ? (c + 1) * GPC : g1;
-#pragma unroll 1
-      for (; g + U <= gend; g += U) {
-        const T* cp = lane_blk + g * 32;
-        T cj[U][NC];
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          T v[U];
-          load_cols<T, U>(cp + k * NTOT, v);
-#pragma unroll
-          for (int u = 0; u < U; ++u) cj[u][k] = v[u];
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) evaluate(cj[u]);
+        for (int k = 0; k < NR; ++k) rv[0][k] = rowbuf[sl * NRMAX + k];
       }
-      if constexpr (U > 1) {
-#pragma unroll 1
-        for (; g < gend; ++g) {
-          const T* cs = lane_one + g * 32;
-          T cj[NC];
-#pragma unroll
-          for (int k = 0; k < NC; ++k) cj[k] = cs[k * NTOT];
-          evaluate(cj);
-        }
-      }
-    }
 
-    // ---- the piece's sums over the lanes (fixed tree), parked for the slot's epilogue threads ----
-    if constexpr (F32) {
+      constexpr int RPK = F32 ? RS / 2 : 1;  // packed row pairs per slot (fp32)
+      T acc[NV];
+      float2 ri2[RPK][NR], acc2[RPK][NA];
+      float2 kexp2, ns2, neg1;
+      if constexpr (F32) {
 #pragma unroll
-      for (int rp = 0; rp < RPK; ++rp)
+        for (int rp = 0; rp < RPK; ++rp) {
 #pragma unroll
-        for (int k = 0; k < NA; ++k) {
-          const bool flip = MODE == kFwd && k < D;  // the packed forward term accumulates -(p_i.p_j) K dx
-          acc[(2 * rp) * NA + k] = (T)(flip ? -acc2[rp][k].x : acc2[rp][k].x);
-          acc[(2 * rp + 1) * NA + k] = (T)(flip ? -acc2[rp][k].y : acc2[rp][k].y);
+          for (int k = 0; k < NR; ++k) {
+            const float lo = (float)rv[2 * rp][k], hi = (float)rv[2 * rp + 1][k];
+            ri2[rp][k] = k < D ? make_float2(-lo, -hi) : make_float2(lo, hi);  // pair_term_packed takes -q_i
+          }
+#pragma unroll
+          for (int k = 0; k < NA; ++k) acc2[rp][k] = make_float2(0.f, 0.f);
         }
-    }
-    int first;
-    unsigned live_mask;
-    LaneTree<T, NV>::run(acc, lane, first, live_mask);
-    if ((lane & live_mask) == 0) {
-      T* mine = part + (pl.pid0 + pc) * NV;
+        kexp2 = splat2((float)a.kexp);
+        ns2 = splat2(-(float)a.inv_sig2);
+        neg1 = splat2(-1.f);
+      } else {
 #pragma unroll
-      for (int j = 0; j < LaneTree<T, NV>::kCount; ++j) mine[first + j] = acc[j];
+        for (int k = 0; k < NV; ++k) acc[k] = T(0);
+      }
+      auto evaluate = [&](const T(&cj)[NC]) {
+        if constexpr (F32) {
+          float2 cj2[NC];
+#pragma unroll
+          for (int k = 0; k < NC; ++k) cj2[k] = splat2((float)cj[k]);
+#pragma unroll
+          for (int rp = 0; rp < RPK; ++rp) pair_term_packed<D, MODE>(ri2[rp], cj2, acc2[rp], kexp2, ns2, neg1);
+        } else {
+          pair_term<T, D, MODE>(rv[0], cj, acc, a.kexp, a.inv_sig2, exp_tbl);
+        }
+      };
+      // The piece chunk by chunk: a chunk is waited for once (they land roughly in order, so everything up to it is
+      // waited for), then its groups are swept without further checks -- blocks of U groups (lane l takes the U
+      // consecutive columns 32 U b + U l ..: one vector load per component), then single groups up to the chunk's
+      // end.  Chunks start at multiples of GPC groups, so only a piece's first chunk can have such a remainder.
+      // Counters and offsets are warp-uniform (uniform datapath: no vector-register reads in the loop control).
+      const T* lane_blk = tile + lane * U;
+      const T* lane_one = tile + lane;
+      int g = g0;
+#pragma unroll 1
+      while (g < g1) {
+        const int c = (int)((unsigned)g / (unsigned)GPC);
+        if (c >= waited) {
+#pragma unroll 1
+          do {
+            mbar_wait_u32(bars_u32 + 8u * (unsigned)waited, (phase_bits >> waited) & 1u);
+            ++waited;
+          } while (waited <= c);
+        }
+        const int gend = (c + 1) * GPC < g1 ? (c + 1) * GPC : g1;
+#pragma unroll 1
+        for (; g + U <= gend; g += U) {
+          const T* cp = lane_blk + g * 32;
+          T cj[U][NC];
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            T v[U];
+            load_cols<T, U>(cp + k * NTOT, v);
+#pragma unroll
+            for (int u = 0; u < U; ++u) cj[u][k] = v[u];
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) evaluate(cj[u]);
+        }
+        if constexpr (U > 1) {
+#pragma unroll 1
+          for (; g < gend; ++g) {
+            const T* cs = lane_one + g * 32;
+            T cj[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) cj[k] = cs[k * NTOT];
+            evaluate(cj);
+          }
+        }
+      }
+
+      // ---- the piece's sums over the lanes (fixed tree), parked for the slot's epilogue threads ----
+      if constexpr (F32) {
+#pragma unroll
+        for (int rp = 0; rp < RPK; ++rp)
+#pragma unroll
+          for (int k = 0; k < NA; ++k) {
+            const bool flip = MODE == kFwd && k < D;  // the packed forward term accumulates -(p_i.p_j) K dx
+            acc[(2 * rp) * NA + k] = (T)(flip ? -acc2[rp][k].x : acc2[rp][k].x);
+            acc[(2 * rp + 1) * NA + k] = (T)(flip ? -acc2[rp][k].y : acc2[rp][k].y);
+          }
+      }
+      int first;
+      unsigned live_mask;
+      LaneTree<T, NV>::run(acc, lane, first, live_mask);
+      if ((lane & live_mask) == 0) {
+        T* mine = part + (win * PMAX + wp.pid0 + pc) * NV;
+#pragma unroll
+        for (int j = 0; j < LaneTree<T, NV>::kCount; ++j) mine[first + j] = acc[j];
+      }
     }
+    // every chunk barrier of this window completed one phase (whether or not this warp waited for it)
+    phase_bits ^= (1u << n_ch) - 1u;
   }
-  phase ^= 1u;  // every chunk barrier completed one phase
+  (void)G;
+  (void)GPW;
   LMS_TRACE_POINT(a, trace_base + 2);
   __syncthreads();
   LMS_TRACE_POINT(a, trace_base + 3);
 
   // ---- epilogue: thread t finishes component t % D of the CTA's row t / D ----
   const int t = threadIdx.x;
-  if (t < pl.s_b * RS * D) {
+  if (t < cx.s_b * RS * D) {
     const int rl = t / D, k = t - rl * D;
     const int sl = rl / RS, h = rl - sl * RS;
-    const long long row = (long long)pl.slot0 * RS + rl;
+    const long long row = (long long)cx.slot0 * RS + rl;
     if (row < a.n) {
-      // the slot's pieces in ascending column order
+      // the slot's pieces in ascending column order: window by window
       T s0 = T(0), s1 = T(0);
-      const T* theirs = part + pl.epi_first * NV + h * NA + k;
 #pragma unroll 1
-      for (int i = 0; i < pl.epi_count; ++i, theirs += NV) {
-        s0 += theirs[0];
-        s1 += theirs[D];
+      for (int win = 0; win < n_windows; ++win) {
+        const SmallEpiPlan ep = cx.eplan[(plan0 + win) * cx.epi_stride + t];
+        const T* theirs = part + (win * PMAX + ep.first) * NV + h * NA + k;
+#pragma unroll 1
+        for (int i = 0; i < ep.count; ++i, theirs += NV) {
+          s0 += theirs[0];
+          s1 += theirs[D];
+        }
       }
       const T* ri = rowbuf + sl * NRMAX * RS + h;  // component c of this row: ri[c * RS]
       if constexpr (MODE == kFwd) {
@@ -548,7 +597,10 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const S
   constexpr int NV = RS * 2 * D;
   extern __shared__ __align__(128) unsigned char small_smem[];
   T* tile = reinterpret_cast<T*>(small_smem);
-  __shared__ __align__(16) T part[kSmallWarps * 2 * NV];               // the pieces' sums
+  __shared__ __align__(16) T part[kSmallMaxWindows * kSmallWarps * kSmallMaxPieces * NV];  // the pieces' sums
+  constexpr int kEpiThreads = kSmallMaxSlots * RS * D;
+  __shared__ SmallWarpPlan wplans[(1 + kSmallMaxWindows) * kSmallWarps];
+  __shared__ SmallEpiPlan eplans[(1 + kSmallMaxWindows) * kEpiThreads];
   __shared__ __align__(16) T rowbuf[kSmallMaxSlots * RS * 4 * D];      // row operands for the epilogue threads
   __shared__ __align__(8) unsigned long long bars[SmallShape<T>::kMaxChunks];
   __shared__ double exp_tbl_all[sizeof(T) == 8 ? kExpTableDoubles : 1];  // fp64 only
@@ -581,8 +633,24 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const S
   small_grid_barrier(a.barrier, bar_target);
   if (bad_input) atomicMin(a.diverged, 0xffffffffull);  // step 0
 
-  const SmallPlan pl = small_plan<RS, D>(a.n);
-  unsigned phase = 0;  // parity the chunk barriers complete next
+  // the work plan of the launch: the forward window, then the one or two adjoint windows (read after the next
+  // __syncthreads: the row staging's)
+  SmallCtx cx;
+  {
+    const int slots = (a.n + RS - 1) / RS;
+    cx.slot0 = (int)((long long)blockIdx.x * slots / gridDim.x);
+    cx.s_b = (int)((long long)(blockIdx.x + 1) * slots / gridDim.x) - cx.slot0;
+    const int G = (a.n + 31) / 32;                    // live 32-column groups
+    constexpr int GPW = SmallShape<T>::kCols / 32;    // ... per adjoint window
+    cx.adj_windows = G > GPW ? 2 : 1;
+    cx.wplan = wplans;
+    cx.eplan = eplans;
+    cx.epi_stride = kEpiThreads;
+    small_plan_window<RS, D>(cx.s_b, G, wplans, eplans);
+    small_plan_window<RS, D>(cx.s_b, G > GPW ? GPW : G, wplans + kSmallWarps, eplans + kEpiThreads);
+    if (G > GPW) small_plan_window<RS, D>(cx.s_b, G - GPW, wplans + 2 * kSmallWarps, eplans + 2 * kEpiThreads);
+  }
+  unsigned phase = 0;  // bit b: parity chunk barrier b completes next
   double hsum = 0.0, msum = 0.0;
   const int Tn = a.timesteps;
   const int lane = threadIdx.x & 31;
@@ -591,7 +659,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const S
   // forward Euler flow, T+1 snapshots kept for the adjoint (shooting.hpp:199-212)
   for (int t = 0; t < Tn; ++t) {
     const unsigned epi = kEpiEuler | (t == 0 ? kEpiFirstStep : 0u) | (t == Tn - 1 ? kEpiLastStep : 0u);
-    small_step<T, D, kFwd, RS>(a, pl, a.traj + (long long)t * a.snap_elems, nullptr, a.traj + (long long)(t + 1) * a.snap_elems,
+    small_step<T, D, kFwd, RS>(a, cx, a.traj + (long long)t * a.snap_elems, nullptr, a.traj + (long long)(t + 1) * a.snap_elems,
                            epi, t + 1, tile, part, rowbuf, bars, phase, hsum, msum, exp_tbl, 8 * t);
     LMS_TRACE_POINT(a, 8 * t + 4);
     if (t == Tn - 1) {
@@ -637,7 +705,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const S
   T* adj_in = a.adj0;
   T* adj_out = a.adj1;
   for (int t = Tn - 1; t >= 0; --t) {
-    small_step<T, D, kAdj, RS>(a, pl, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
+    small_step<T, D, kAdj, RS>(a, cx, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
                            kEpiEuler | (t == 0 ? kEpiGradOut : 0u), t, tile, part, rowbuf, bars, phase, hsum, msum,
                            exp_tbl, 8 * (2 * Tn - 1 - t));
     LMS_TRACE_POINT(a, 8 * (2 * Tn - 1 - t) + 4);

@@ -493,8 +493,8 @@ void System<T, D>::plan_small()
   int coop = 0;
   LMS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cfg.device));
   if (!coop) return;
-  // one contiguous array of kCols columns per component; the last one only as long as the staged chunks
-  small_smem_ = ((size_t)(4 * D - 1) * SmallShape<T>::kCols + (size_t)ceil_div(n(), CH) * CH) * sizeof(T);
+  // one window: 4D components of kCols columns (adjoint) = 2D components of twice as many (forward)
+  small_smem_ = (size_t)(4 * D) * SmallShape<T>::kCols * sizeof(T);
   LMS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(small_fn_), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)small_smem_));
   int per_sm = 0;

@@ -121,12 +121,14 @@ def test_compute_gradient_parity(hs, oracle, prec, n, T, lam, tiled_only):
 @pytest.mark.parametrize("prec", ["f32", "f64"])
 @pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 31, 32, 33, 255, 256, 257, 295, 296, 297, 511, 512, 513, 1000, 1184, 1185, 2047, 2048,
-                               2049, 2369, 2900, 4095, 4096, 4097])
+                               2049, 2369, 2900, 3400, 3401, 4095, 4096, 4097, 4737, 8191, 8192, 8193])
 def test_persistent_kernel_edge_sizes(hs, oracle, prec, dim, n):
     """The persistent path at the sizes where its decomposition changes: fewer rows than one slot, fewer work items
-    than warps, one chunk of staged columns +- 1 (512 fp32 / 256 fp64), one slot per CTA +- 1 (148 SMs x 2 rows),
-    several slots per CTA (a warp's run then spans two slots), the shared-memory capacity +- 1 (4096 fp32 / 2048
-    fp64), an odd last row of a packed pair; odd T and even T end in different adjoint buffers.  Checked against the
+    than warps, one chunk of staged columns +- 1 (2048 fp32 / 1024 fp64), one slot per CTA +- 1 (148 SMs x 2 rows),
+    several slots per CTA (a warp's run then spans two or three slots: 4737 is the first size with more than 16),
+    one adjoint window +- 1 (4096 fp32 / 2048 fp64: above it the adjoint sweep stages two windows per step), the
+    largest size it is chosen for +- 1 (8192 fp32, the capacity; 3400 fp64, the crossover with the tiled path), an
+    odd last row of a packed pair; odd T and even T end in different adjoint buffers.  Checked against the
     oracle, against the tiled path (same epilogue arithmetic, different summation order) and for run-to-run bits."""
     tol = TOL[prec]
     # constant landmark density (a denser cloud than ~500 per 14^dim box makes the flow itself ill-conditioned in fp32)
@@ -135,8 +137,8 @@ def test_persistent_kernel_edge_sizes(hs, oracle, prec, dim, n):
     tiled = hs(n, dim, prec, max_t=8, tiled_only=True)
     for T in (3, 4):
         r = s.compute_gradient(q, p, target, 25.0, T)
-        # the persistent kernel holds the whole state in shared memory: up to 4096 landmarks in fp32, 2048 in fp64
-        assert s.last_eval_kernel_launches() == (1 if n <= (4096 if prec == "f32" else 2048) else 2 * T + 2)
+        # the persistent kernel stages the state in shared memory: chosen up to 8192 landmarks in fp32, 3400 in fp64
+        assert s.last_eval_kernel_launches() == (1 if n <= (8192 if prec == "f32" else 3400) else 2 * T + 2)
         loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, SIGMA, 25.0, T)
         assert r.loss == pytest.approx(loss, rel=tol) and r.kinetic == pytest.approx(kin, rel=tol, abs=1e-300)
         assert r.mismatch == pytest.approx(mm, rel=tol)
@@ -153,16 +155,18 @@ def test_persistent_kernel_edge_sizes(hs, oracle, prec, dim, n):
 @pytest.mark.parametrize("prec", ["f32", "f64"])
 @pytest.mark.parametrize("n", [4500, 6100, 8200, 11000])
 def test_mid_size_parity(hs, oracle, prec, n):
-    """Mid-size single problems, where the launch machinery differs from both ends of the range: programmatic
-    dependent launch between the pair kernels (below 8000 landmarks), the combine's shared-memory landing zone (at
-    most two CTAs per SM, up to 20 partial segments per row tile), two-row shapes below 8000, four-row shapes above
-    unless they pad more than they gain (11 000).  Against the oracle, and bitwise run to run."""
+    """Mid-size single problems, where the machinery differs from both ends of the range: the persistent kernel with
+    two adjoint windows per step (fp32 up to 8192), and on the tiled path programmatic dependent launch between the pair
+    kernels (below 8000 landmarks), the combine's shared-memory landing zone (at most two CTAs per SM, up to 20
+    partial segments per row tile), four-row shapes from 8000 on unless they pad more than they gain (11 000).
+    Against the oracle, and bitwise run to run."""
     tol = TOL[prec]
     T, lam = 3, 50.0
     q, p, target, *_ = synth_case(n, 3, 5000 + n, spread=7.0 * (n / 500.0) ** (1.0 / 3))
     s = hs(n, 3, prec, max_t=4)
     r = s.compute_gradient(q, p, target, lam, T)
-    assert s.last_eval_kernel_launches() == 2 * T + 2
+    persistent = n <= (8192 if prec == "f32" else 3400)  # the persistent kernel's range (two adjoint windows above 4096 / 2048)
+    assert s.last_eval_kernel_launches() == (1 if persistent else 2 * T + 2)
     loss, kin, mm, grad = oracle.compute_gradient(prec, q, p, target, SIGMA, lam, T)
     assert r.loss == pytest.approx(loss, rel=tol) and r.kinetic == pytest.approx(kin, rel=tol)
     assert r.mismatch == pytest.approx(mm, rel=tol)
@@ -557,11 +561,11 @@ def test_registration_metrics_on_device(hs, oracle, prec, n, dim):
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-@pytest.mark.parametrize("n", [700, 6000])
+@pytest.mark.parametrize("n", [700, 6000, 9000])
 def test_host_and_device_buffer_calls_agree(hs, prec, n):
     """lms_objective_eval (host buffers; the persistent kernel reads / writes them in place through mapped pinned
     memory) and lms_objective_eval_device (x / grad in HBM) are the same evaluation: bitwise equal loss, H, mismatch
-    and gradient, in either order, for a persistent-size and a tiled-size problem; a non-finite x is DivergedError(0)
+    and gradient, in either order, for persistent-size (one and two adjoint windows) and tiled-size problems; a non-finite x is DivergedError(0)
     through both."""
     import torch
 
