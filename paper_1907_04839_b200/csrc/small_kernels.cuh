@@ -261,46 +261,45 @@ struct SmallEpiPlan {  // epilogue thread: its slot's pieces of that window are 
   int first, count;
 };
 
-// The work list of one window (s_b slots x Gw groups, slot-major) cut into sixteen equal contiguous runs.  Every
-// thread walks the sixteen runs: lane 0 of a warp records the warp's run, epilogue thread t (component t % D of the
-// CTA's row t / D) where its slot's pieces lie.
+// The work list of one window (s_b slots x Gw groups, slot-major) cut into sixteen equal contiguous runs.  Two
+// phases around one __syncthreads, so that the integer divisions are done once per run and not by every thread (the
+// plan is worked out once per launch, but on a 0.1 ms evaluation a few microseconds count): thread w < 16 describes
+// run w; then lane 0 of every warp records its warp's pieces and epilogue thread t (component t % D of the CTA's
+// row t / D) finds where its slot's pieces lie.
+struct SmallRun {
+  int r0, r1;  // items [r0, r1) of the window's work list
+  int s0, s1;  // first and last slot touched (s1 <= s0 + 2); r1 == r0: an empty run (fewer items than warps)
+};
 template <int RS, int D>
-__device__ __forceinline__ void small_plan_window(int s_b, int Gw, SmallWarpPlan* wplan, SmallEpiPlan* eplan)
+__device__ __forceinline__ void small_plan_window(int Gw, const SmallRun* runs, SmallWarpPlan* wplan, SmallEpiPlan* eplan)
 {
   const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
-  const int total = s_b * Gw;
-  const int my_slot = (int)threadIdx.x / (RS * D);
-  SmallWarpPlan mine;
-  mine.n_pieces = 0;
-  mine.pid0 = 0;
+  if (lane == 0) {
+    SmallWarpPlan mine;
+    const SmallRun r = runs[warp];
+    mine.n_pieces = r.s1 - r.s0 + 1;  // 0 for an empty run
+    mine.pid0 = 0;
+    for (int w = 0; w < warp; ++w) mine.pid0 += runs[w].s1 - runs[w].s0 + 1;
 #pragma unroll
-  for (int j = 0; j < kSmallMaxPieces; ++j) mine.sl[j] = mine.g0[j] = mine.g1[j] = 0;
-  int first = 0, count = 0, pid = 0;
-  for (int w = 0; w < kSmallWarps; ++w) {
-    const int r0 = w * total / kSmallWarps, r1 = (w + 1) * total / kSmallWarps;
-    if (r1 == r0) continue;  // fewer items than warps
-    const int s0 = r0 / Gw, s1 = (r1 - 1) / Gw;  // s1 <= s0 + 2: a run is at most 2 Gw items long
-    if (w == warp) {
-      mine.n_pieces = s1 - s0 + 1;
-      mine.pid0 = pid;
-#pragma unroll
-      for (int j = 0; j < kSmallMaxPieces; ++j) {
-        const int sl = s0 + j;
-        if (sl <= s1) {
-          mine.sl[j] = sl;
-          mine.g0[j] = j == 0 ? r0 - s0 * Gw : 0;
-          mine.g1[j] = sl == s1 ? r1 - s1 * Gw : Gw;
-        }
+    for (int j = 0; j < kSmallMaxPieces; ++j) {
+      const int sl = r.s0 + j;
+      const bool on = sl <= r.s1;
+      mine.sl[j] = on ? sl : 0;
+      mine.g0[j] = on && j == 0 ? r.r0 - r.s0 * Gw : 0;
+      mine.g1[j] = on ? (sl == r.s1 ? r.r1 - r.s1 * Gw : Gw) : 0;
+    }
+    wplan[warp] = mine;
+  }
+  if ((int)threadIdx.x < kSmallMaxSlots * RS * D) {
+    const int my_slot = (int)threadIdx.x / (RS * D);
+    int first = 0, count = 0;
+    for (int w = 0; w < kSmallWarps; ++w) {
+      const int s0 = runs[w].s0, s1 = runs[w].s1;
+      for (int sl = s0; sl <= s1; ++sl) {
+        if (sl < my_slot) ++first;
+        if (sl == my_slot) ++count;
       }
     }
-    for (int sl = s0; sl <= s1; ++sl) {
-      if (sl < my_slot) ++first;
-      if (sl == my_slot) ++count;
-    }
-    pid += s1 - s0 + 1;
-  }
-  if (lane == 0) wplan[warp] = mine;
-  if ((int)threadIdx.x < kSmallMaxSlots * RS * D) {
     eplan[threadIdx.x].first = first;
     eplan[threadIdx.x].count = count;
   }
@@ -318,7 +317,7 @@ struct SmallCtx {
 
 // One time step for this CTA's rows.  MODE kFwd: state -> out = next snapshot (Euler, shooting.hpp:205-211) with
 // the first / last step extras; MODE kAdj: (state, adj_in) -> out = next adjoint state (:302-306).
-template <typename T, int D, int MODE, int RS>
+template <typename T, int D, int MODE, int RS, int MAXW>
 __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallCtx& cx, const T* __restrict__ state,
                                            const T* __restrict__ adj_in, T* __restrict__ out, unsigned epi, int step_no,
                                            T* tile, T* part, T* rowbuf, unsigned long long* bars, unsigned& phase_bits,
@@ -338,8 +337,10 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallCtx
   constexpr int PMAX = kSmallWarps * kSmallMaxPieces;  // pieces per window
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int n_windows = MODE == kAdj ? cx.adj_windows : 1;
-  const int plan0 = MODE == kAdj ? 1 : 0;
+  // MAXW == 1: the whole state fits one adjoint window (N <= 4096 fp32 / 2048 fp64): no window loop, and the forward
+  // and adjoint sweeps share one work plan
+  const int n_windows = (MODE == kAdj && MAXW > 1) ? cx.adj_windows : 1;
+  const int plan0 = (MODE == kAdj && MAXW > 1) ? 1 : 0;
   const int G = (a.n + 31) / 32;  // live groups
 
   auto plane = [&](int k) -> const T* {
@@ -590,17 +591,19 @@ __device__ __forceinline__ void small_step(const SmallArgs<T>& a, const SmallCtx
   }
 }
 
-template <typename T, int D, int RS = SmallShape<T>::kRowsPerSlot>
+template <typename T, int D, int MAXW = kSmallMaxWindows, int RS = SmallShape<T>::kRowsPerSlot>
 __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const SmallArgs<T> a)
 {
   constexpr int kThreadsHere = 32 * kSmallWarps;
   constexpr int NV = RS * 2 * D;
   extern __shared__ __align__(128) unsigned char small_smem[];
   T* tile = reinterpret_cast<T*>(small_smem);
-  __shared__ __align__(16) T part[kSmallMaxWindows * kSmallWarps * kSmallMaxPieces * NV];  // the pieces' sums
+  __shared__ __align__(16) T part[MAXW * kSmallWarps * kSmallMaxPieces * NV];  // the pieces' sums
   constexpr int kEpiThreads = kSmallMaxSlots * RS * D;
-  __shared__ SmallWarpPlan wplans[(1 + kSmallMaxWindows) * kSmallWarps];
-  __shared__ SmallEpiPlan eplans[(1 + kSmallMaxWindows) * kEpiThreads];
+  constexpr int kPlans = MAXW > 1 ? 1 + MAXW : 1;  // forward + adjoint windows, or one shared plan
+  __shared__ SmallWarpPlan wplans[kPlans * kSmallWarps];
+  __shared__ SmallRun runs[kPlans * kSmallWarps];
+  __shared__ SmallEpiPlan eplans[(MAXW > 1 ? 1 + MAXW : 1) * kEpiThreads];
   __shared__ __align__(16) T rowbuf[kSmallMaxSlots * RS * 4 * D];      // row operands for the epilogue threads
   __shared__ __align__(8) unsigned long long bars[SmallShape<T>::kMaxChunks];
   __shared__ double exp_tbl_all[sizeof(T) == 8 ? kExpTableDoubles : 1];  // fp64 only
@@ -642,13 +645,36 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const S
     cx.s_b = (int)((long long)(blockIdx.x + 1) * slots / gridDim.x) - cx.slot0;
     const int G = (a.n + 31) / 32;                    // live 32-column groups
     constexpr int GPW = SmallShape<T>::kCols / 32;    // ... per adjoint window
-    cx.adj_windows = G > GPW ? 2 : 1;
+    cx.adj_windows = (MAXW > 1 && G > GPW) ? 2 : 1;
     cx.wplan = wplans;
     cx.eplan = eplans;
     cx.epi_stride = kEpiThreads;
-    small_plan_window<RS, D>(cx.s_b, G, wplans, eplans);
-    small_plan_window<RS, D>(cx.s_b, G > GPW ? GPW : G, wplans + kSmallWarps, eplans + kEpiThreads);
-    if (G > GPW) small_plan_window<RS, D>(cx.s_b, G - GPW, wplans + 2 * kSmallWarps, eplans + 2 * kEpiThreads);
+    // plan 0: the forward window (all G groups); with MAXW > 1 plans 1, 2: the adjoint windows (the first GPW groups, the
+    // rest); with MAXW == 1 the host guarantees G <= GPW and the adjoint sweep uses plan 0 as well
+    int gw[kPlans];
+    gw[0] = G;
+    if constexpr (MAXW > 1) {
+      gw[1] = G > GPW ? GPW : G;
+      gw[2] = G > GPW ? G - GPW : 0;
+    }
+    const int pl = (int)threadIdx.x / kSmallWarps, w = (int)threadIdx.x - pl * kSmallWarps;
+    if (pl < kPlans) {
+      const int gwp = pl == 0 ? gw[0] : (pl == 1 ? gw[kPlans > 1 ? 1 : 0] : gw[kPlans > 2 ? 2 : 0]);
+      if (gwp > 0) {
+        const int total = cx.s_b * gwp;
+        SmallRun r;
+        r.r0 = w * total / kSmallWarps;
+        r.r1 = (w + 1) * total / kSmallWarps;
+        r.s0 = r.r1 > r.r0 ? r.r0 / gwp : 0;
+        r.s1 = r.r1 > r.r0 ? (r.r1 - 1) / gwp : -1;
+        runs[pl * kSmallWarps + w] = r;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int p2 = 0; p2 < kPlans; ++p2)
+      if (gw[p2] > 0)
+        small_plan_window<RS, D>(gw[p2], runs + p2 * kSmallWarps, wplans + p2 * kSmallWarps, eplans + p2 * kEpiThreads);
   }
   unsigned phase = 0;  // bit b: parity chunk barrier b completes next
   double hsum = 0.0, msum = 0.0;
@@ -659,7 +685,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const S
   // forward Euler flow, T+1 snapshots kept for the adjoint (shooting.hpp:199-212)
   for (int t = 0; t < Tn; ++t) {
     const unsigned epi = kEpiEuler | (t == 0 ? kEpiFirstStep : 0u) | (t == Tn - 1 ? kEpiLastStep : 0u);
-    small_step<T, D, kFwd, RS>(a, cx, a.traj + (long long)t * a.snap_elems, nullptr, a.traj + (long long)(t + 1) * a.snap_elems,
+    small_step<T, D, kFwd, RS, MAXW>(a, cx, a.traj + (long long)t * a.snap_elems, nullptr, a.traj + (long long)(t + 1) * a.snap_elems,
                            epi, t + 1, tile, part, rowbuf, bars, phase, hsum, msum, exp_tbl, 8 * t);
     LMS_TRACE_POINT(a, 8 * t + 4);
     if (t == Tn - 1) {
@@ -705,7 +731,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 1) small_eval_kernel(const S
   T* adj_in = a.adj0;
   T* adj_out = a.adj1;
   for (int t = Tn - 1; t >= 0; --t) {
-    small_step<T, D, kAdj, RS>(a, cx, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
+    small_step<T, D, kAdj, RS, MAXW>(a, cx, a.traj + (long long)t * a.snap_elems, adj_in, adj_out,
                            kEpiEuler | (t == 0 ? kEpiGradOut : 0u), t, tile, part, rowbuf, bars, phase, hsum, msum,
                            exp_tbl, 8 * (2 * Tn - 1 - t));
     LMS_TRACE_POINT(a, 8 * (2 * Tn - 1 - t) + 4);

@@ -488,7 +488,8 @@ void System<T, D>::plan_small()
   // so any slot count up to kSmallMaxSlots keeps every warp busy.  (Before: one slot per row warp, the spare warps
   // splitting the columns evenly -- N = 3000 left 5 of 16 warps idle.)
   if (ceil_div(slots, grid) > kSmallMaxSlots) return;
-  small_fn_ = small_eval_kernel<T, D>;
+  // one adjoint window (N <= 4096 fp32 / 2048 fp64): the instantiation without the window loop
+  small_fn_ = n() <= SmallShape<T>::kCols ? small_eval_kernel<T, D, 1> : small_eval_kernel<T, D>;
   small_threads_ = 32 * kSmallWarps;
   int coop = 0;
   LMS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cfg.device));

@@ -33,10 +33,15 @@ for prec in ("f32", "f64"):
         reg = register_landmarks(q, tg, ShootingConfig(sigma=1.5, timesteps=T, lam=100.0, max_iter=4, precision=prec),
                                  device_vectors=dv)
         print("registration, device vectors" if dv else "registration, host driver", reg.final_loss, reg.avg_after)
-    # a mid-size problem: programmatic dependent launch, the combine's shared-memory landing zone with many segments
+    # the persistent kernel with two adjoint windows per step (fp32: above 4096 landmarks; fp64: above 2048)
+    nw = 4600 if prec == "f32" else 2300
+    qw = rng.uniform(-14, 14, (nw, 3)); pw = rng.normal(size=(nw, 3)); tw = qw + 0.3 * rng.normal(size=(nw, 3))
+    s = HamiltonianSystem(1.5, nw, 3, prec, max_timesteps=2)
+    print("two windows", s.compute_gradient(qw, pw, tw, 10.0, 2).loss, s.last_eval_kernel_launches()); s.close()
+    # a mid-size problem on the tiled path: programmatic dependent launch, the combine's shared-memory landing zone
     n5 = 4500
     q5 = rng.uniform(-14, 14, (n5, 3)); p5 = rng.normal(size=(n5, 3)); t5k = q5 + 0.3 * rng.normal(size=(n5, 3))
-    s = HamiltonianSystem(1.5, n5, 3, prec, max_timesteps=2)
+    s = HamiltonianSystem(1.5, n5, 3, prec, max_timesteps=2, tiled_only=True)
     print("mid-size", s.compute_gradient(q5, p5, t5k, 10.0, 2).loss, s.last_eval_kernel_launches()); s.close()
     # (the in-process peer-push test is left out: compute-sanitizer serialises kernel launches of the process, so
     #  a rank's stream-ordered wait for its peer's flag blocks the very launch that would set it)
