@@ -54,8 +54,8 @@ typedef struct lms_config {
   int flags;         /* 0, or LMS_FLAG_* bits */
 } lms_config;
 
-/* Small single problems run the whole evaluation as one persistent cooperative kernel (csrc/small_kernels.cuh);
- * this bit pins the tiled multi-launch path instead (A/B and tests). */
+/* Single problems of up to 8192 landmarks in fp32 (3400 in fp64) run the whole evaluation as one persistent
+ * cooperative kernel (csrc/small_kernels.cuh); this bit pins the tiled multi-launch path instead (A/B and tests). */
 #define LMS_FLAG_TILED_ONLY 1
 
 int lms_system_create(const lms_config* cfg, lms_system** out);
