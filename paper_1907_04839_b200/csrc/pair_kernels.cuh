@@ -43,6 +43,8 @@ constexpr int kMaxPeers = 7;   // row partition, peer-push transport: up to 8 GP
 constexpr int kMaxRanks = 64;  // row partition, any transport (the in-process loopback group takes up to 64)
 
 enum Mode : int { kFwd = 0, kAdj = 1, kVel = 2 };
+template <bool B>
+struct ThinTag { static constexpr bool value = B; };
 
 // Epilogue selector / flags.
 enum : unsigned {
@@ -68,6 +70,16 @@ struct PairArgs {
   int n_rows;       // rows are valid for row < n_rows
   int row_tile0;    // first row tile owned by this launch (row partition across GPUs)
   int n_row_tiles;  // row tiles owned by this launch
+  // Thin last row tile: when the launch's last row tile holds at most 1/thin_split of a tile's rows (the rest is
+  // padding), its live rows are replicated over thin_split groups of warps and each group sweeps 1/thin_split of
+  // every staged column tile; the groups' sums meet in shared memory before the stream-K combine.  The tile then
+  // counts 1/thin_split of a tile's work units.  1: every tile is a full tile.  (2 or 4; single problem only.)
+  int thin_split;
+  // A thin tile stages a whole column tile for 1/thin_split of the work, so its units cost a few per cent more than a
+  // full tile's, and the CTAs sweeping it would finish last.  To keep the stream-K shares equal in time, every
+  // thin_period-th cell of the thin tile is a phantom (no columns): the tile counts P + P / (thin_period - 1) cells
+  // for its P units.  0: no phantoms.
+  int thin_period;
   // outputs
   T* out;           // raw: sums planes; euler: next state / next adjoint state / moved points
   long long ostride;
@@ -400,12 +412,14 @@ __device__ __forceinline__ void pair_term_packed(const float2* __restrict__ ri2,
 
 // Row owned by (r, tid) in row tile rt.  Packed kernels pair rows (2*tid, 2*tid+1) of each 256-row group.
 template <int R, bool PACKED>
-__device__ __forceinline__ long long row_of(int rt, int r, int tid)
+__device__ __forceinline__ long long row_of(int rt, int r, int tid, int threads = kThreads)
 {
+  // `threads` < kThreads: a thin tile (PairArgs::thin_split), whose rows are laid over the first `threads`
+  // threads only (tid is then the index within that group)
   if constexpr (PACKED)
-    return (long long)rt * (kThreads * R) + (r >> 1) * (2 * kThreads) + 2 * tid + (r & 1);
+    return (long long)rt * (kThreads * R) + (r >> 1) * (2 * threads) + 2 * tid + (r & 1);
   else
-    return (long long)rt * (kThreads * R) + r * kThreads + tid;
+    return (long long)rt * (kThreads * R) + r * threads + tid;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -510,7 +524,7 @@ __device__ __forceinline__ double block_sum(double v, double* scratch)
 // its sums in its own tile buffers, rank 0 adds the kClusterSize copies in ascending column order and runs the
 // epilogue) instead of going through global slots, a fence, an arrival counter and L2 round trips.
 template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false,
-          bool AOS = false, bool CLUSTER = false, bool PEERS = false>
+          bool AOS = false, bool CLUSTER = false, bool PEERS = false, bool THINOK = false>
 __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> a)
 {
   static_assert(!CLUSTER || 2 * Shape<MODE, D>::kColComps * kTileJ >= Shape<MODE, D>::kAcc * kThreads * R,
@@ -566,19 +580,29 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
   // Work is counted in units of kUnitJ columns of one row tile, so every CTA's share differs by at most
   // one unit (1/16 of a staged tile); `cells` and `nJ` below are in those units.
   const long long nJ = (long long)a.n_j_tiles * kUnitsPerTile;
-  const long long cells = (long long)a.n_row_tiles * nJ;
+  // (THINOK: only the shapes instantiated with the thin-tile code take it; the others compile as if it did not exist)
+  const int split = THINOK && a.thin_split > 1 ? a.thin_split : 1;  // > 1: the last row tile is thin and holds fewer units
+  const int period = split > 1 && a.thin_period > 1 ? a.thin_period : 0;
+  const long long nJ_thin = nJ / split + (period ? (nJ / split) / (period - 1) : 0);  // cells of the thin tile
+  const long long cells = (long long)a.n_row_tiles * nJ - (nJ - nJ_thin);
   const long long G = gridDim.x;
   long long c = cells * blockIdx.x / G;
   const long long c_end = cells * (blockIdx.x + 1) / G;
 
   while (c < c_end) {
-    const long long rt_local = c / nJ;
-    const int u0 = (int)(c - rt_local * nJ);  // unit range [u0, u1) of this row tile
+    const long long rt_local = c / nJ;  // (the thin tile is the last one, so this holds for it too)
+    const bool thin = THINOK && split > 1 && rt_local == a.n_row_tiles - 1;
+    const long long nJ_this = thin ? nJ_thin : nJ;
+    const int tc0 = (int)(c - rt_local * nJ);  // cell range [tc0, tc1) of this row tile
     const long long span = c_end - c;
-    const int u1 = (int)((long long)u0 + span < nJ ? (long long)u0 + span : nJ);
-    const int col0 = u0 * kUnitJ, col1 = u1 * kUnitJ;  // column range, multiples of kUnitJ
-    const int jt0 = col0 / kTileJ;
-    const int jt1 = (col1 + kTileJ - 1) / kTileJ;
+    const int tc1 = (int)((long long)tc0 + span < nJ_this ? (long long)tc0 + span : nJ_this);
+    // Unit range of the cells [tc0, tc1): the cells themselves, minus the phantoms before them in a thin tile.  A
+    // unit is kUnitJ columns per sweeping group of warps.  Full tile: one group (the CTA), kUnitsPerTile units per
+    // staged tile.  Thin tile: `split` groups side by side, group g sweeping columns [g, g + 1) * kTileJ / split of
+    // every staged tile, so a staged tile holds kUnitsPerTile / split units.  (Everything thin-specific is derived
+    // from tc0 / tc1 where it is used, so that full tiles carry nothing extra through their sweep.)
+    auto units_of = [&](int tc) { return period ? tc - tc / period : tc; };
+    const int jt_first = thin ? units_of(tc0) / (kUnitsPerTile / split) : tc0 * kUnitJ / kTileJ;  // first staged tile
     // problem this row tile belongs to (uniform per CTA iteration: lives in uniform registers)
     const long long bc = rt_local / a.tiles_per_problem;
     const long long prob = a.batch_ids != nullptr ? (long long)a.batch_ids[bc] : bc;
@@ -608,7 +632,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     T ri[R][NR];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const long long row = row_of<R, PACKED>(rt, r, tid);
+      const int grp_threads = thin ? kThreads / split : kThreads;  // threads that hold distinct rows
+      const long long row = thin ? row_of<R, PACKED>(rt, r, tid % grp_threads, grp_threads) : row_of<R, PACKED>(rt, r, tid);
 #pragma unroll
       for (int k = 0; k < NR; ++k) {
         if constexpr (MODE == kAdj) {
@@ -626,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       for (int k = 0; k < NA; ++k) acc[r][k] = T(0);
 
     // ---- sweep the j tiles [jt0, jt1) with register-prefetched double buffering ---------------
-    // (only columns [col0, col1) of the first and last tile are accumulated)
+    // (only the units [u0, u1) of the first and last tile are accumulated)
     T stage[BULK ? 1 : NC];
     auto issue_tile = [&](int jt, int b) {  // BULK: called by thread 0 only
       mbar_expect_tx(&tile_bar[b], (unsigned)(NC * kTileJ * sizeof(T)));
@@ -635,10 +660,11 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         bulk_g2s(&tile[b][k][0], col_plane(k) + (long long)jt * kTileJ, (unsigned)(kTileJ * sizeof(T)), &tile_bar[b]);
     };
     if constexpr (BULK) {
-      if (tid == 0) issue_tile(jt0, buf);  // buffer `buf` was last read before the previous __syncthreads
+      // (a thin range that is a single phantom cell sweeps nothing: tc1 - tc0 > 1 or the cell is a real one)
+      if (tid == 0 && (!thin || units_of(tc1) > units_of(tc0))) issue_tile(jt_first, buf);  // `buf` was last read before the previous __syncthreads
     } else {
 #pragma unroll
-      for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)jt0 * kTileJ + tid];
+      for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)jt_first * kTileJ + tid];
       buf = 0;
 #pragma unroll
       for (int k = 0; k < NC; ++k) {
@@ -669,6 +695,19 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       neg1 = splat2(-1.f);
     }
 
+    // The sweep is instantiated twice: the full-tile copy has its column bounds in compile-time multiples of the
+    // tile (the hot loop of every launch, code-generated exactly as before the thin tile existed), the thin copy
+    // takes the group's column window and units-per-tile from registers.
+    auto sweep = [&](auto thin_tag) {
+    constexpr bool THIN = decltype(thin_tag)::value;
+    // full tile: the column range [col0, col1) in multiples of kUnitJ, as compile-time-scaled integers
+    const int col0 = tc0 * kUnitJ, col1 = tc1 * kUnitJ;
+    const int upt_s = kUnitsPerTile / split;
+    const int u0 = THIN ? units_of(tc0) : 0;
+    const int u1 = THIN ? units_of(tc1) : 0;
+    const int jt0 = THIN ? u0 / upt_s : col0 / kTileJ;
+    const int jt1 = THIN ? (u1 > u0 ? (u1 + upt_s - 1) / upt_s : jt0) : (col1 + kTileJ - 1) / kTileJ;
+    const int jj_base = THIN ? (tid / (kThreads / split)) * (kTileJ / split) : 0;  // this group's window of a tile
     for (int jt = jt0; jt < jt1; ++jt) {
       const bool more = jt + 1 < jt1;
       if constexpr (BULK) {
@@ -681,8 +720,16 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
           for (int k = 0; k < NC; ++k) stage[k] = col_plane(k)[(long long)(jt + 1) * kTileJ + tid];
         }
       }
-      const int jj_lo = col0 > jt * kTileJ ? col0 - jt * kTileJ : 0;
-      const int jj_hi = col1 < (jt + 1) * kTileJ ? col1 - jt * kTileJ : kTileJ;
+      int jj_lo, jj_hi;
+      if constexpr (THIN) {
+        const int k_lo = u0 > jt * upt_s ? u0 - jt * upt_s : 0;
+        const int k_hi = u1 < (jt + 1) * upt_s ? u1 - jt * upt_s : upt_s;
+        jj_lo = jj_base + k_lo * kUnitJ;
+        jj_hi = jj_base + k_hi * kUnitJ;
+      } else {
+        jj_lo = col0 > jt * kTileJ ? col0 - jt * kTileJ : 0;
+        jj_hi = col1 < (jt + 1) * kTileJ ? col1 - jt * kTileJ : kTileJ;
+      }
 #pragma unroll UNR
       for (int jj = jj_lo; jj < jj_hi; jj += JU) {
         T cj[JU][NC];
@@ -731,6 +778,13 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       __syncthreads();
       buf ^= 1;
     }
+    };
+    if constexpr (THINOK) {
+      if (thin) sweep(ThinTag<true>{});
+      else sweep(ThinTag<false>{});
+    } else {
+      sweep(ThinTag<false>{});
+    }
     if constexpr (PACKED) {
       // back to the scalar convention of pair_term: forward acc[0..D) holds +(p_i.p_j) K dx.  The scalar
       // row operands are rebuilt from the packed ones so that only one copy stays live across the sweep.
@@ -751,8 +805,30 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     }
 
     // ---- combine partial sums across the CTAs that share this row tile ----------------------------
+    // (recomputed here rather than kept in registers across the sweep)
+    const int grp_threads = thin ? kThreads / split : kThreads;   // threads that hold distinct rows
+    const int grp = thin ? tid / grp_threads : 0;                 // column group of this thread (warp-uniform)
+    const int gtid = tid - grp * grp_threads;                     // its index within the group
+    if (thin) {
+      // the `split` column groups hold partial sums of the same rows: group 0 adds them in ascending group
+      // (= ascending column-within-tile) order, one accumulator at a time through the reduction scratch
+      T* red = reinterpret_cast<T*>(red_scratch);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+          red[tid] = acc[r][k];
+          __syncthreads();
+          if (grp == 0) {
+            T v = acc[r][k];
+            for (int g = 1; g < split; ++g) v += red[g * grp_threads + gtid];
+            acc[r][k] = v;
+          }
+          __syncthreads();
+        }
+    }
     const long long cell_lo = rt_local * nJ;
-    const long long cell_hi = cell_lo + nJ - 1;
+    const long long cell_hi = cell_lo + nJ_this - 1;
     const long long cta_first = ((cell_lo + 1) * G - 1) / cells;
     const long long cta_last = ((cell_hi + 1) * G - 1) / cells;
     bool do_epilogue = true;
@@ -868,8 +944,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       double hsum = 0.0, msum = 0.0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const long long row = row_of<R, PACKED>(rt, r, tid);
-        const bool live = row < a.n_rows;
+        const long long row = row_of<R, PACKED>(rt, r, gtid, grp_threads);
+        const bool live = row < a.n_rows && grp == 0;  // thin tile: group 0 holds the sums
         if constexpr (MODE == kVel) {
           if (live) {
             if (a.epi & kEpiEuler) {
@@ -970,7 +1046,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         }
       }
     }
-    c += u1 - u0;
+    c += tc1 - tc0;
   }
 }
 

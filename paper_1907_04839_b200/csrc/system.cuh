@@ -127,15 +127,17 @@ struct KernelChoice {
   void (*fn_cluster)(PairArgs<T>) = nullptr;  // same shape with the cluster combine (small problems), or null
   void (*fn_peers)(PairArgs<T>) = nullptr;    // same shape with the peer-push stores in its epilogues (row partition), or null
   int rows_per_thread = 0;
+  bool thin_ok = false;  // fn carries the thin-last-row-tile code (PairArgs::thin_split)
   const char* name = "";
 };
 
 template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = false, int UNR = 1, bool BULK = false,
-          bool AOS = false, bool WITH_CLUSTER = false, bool WITH_PEERS = false>
+          bool AOS = false, bool WITH_CLUSTER = false, bool WITH_PEERS = false, bool WITH_THIN = false>
 KernelChoice<T> make_choice(const char* name)
 {
   KernelChoice<T> c;
-  c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS>;
+  c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, false, false, WITH_THIN>;
+  c.thin_ok = WITH_THIN;
   if constexpr (WITH_CLUSTER) c.fn_cluster = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, true>;
   if constexpr (WITH_PEERS) c.fn_peers = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, false, true>;
   c.rows_per_thread = R;
@@ -162,6 +164,8 @@ struct LaunchPlan {
   int n_row_tiles = 0;
   int n_j_tiles = 0;
   int tiles_per_problem = 1;
+  int thin_split = 1;  // > 1: the last row tile is thin (PairArgs::thin_split)
+  int thin_period = 0; // phantom-cell period of the thin tile (PairArgs::thin_period)
   bool cluster = false;  // launch fn_cluster as clusters of kClusterSize CTAs, one cluster per row tile
   int bm = 0;
   size_t partial_elems = 0;

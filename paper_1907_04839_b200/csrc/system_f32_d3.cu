@@ -21,7 +21,7 @@ KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
   switch (v) {
     case 1: return make_choice<float, 3, kFwd, 4, 4, 3>("fwd_f32_r4_j4");
     case 11: return make_choice<float, 3, kFwd, 2, 4, 7, true>("fwd_f32x2_r2_j4_b7");
-    case 25: return make_choice<float, 3, kFwd, 4, 4, 3, true, 2, true, false, false, true>("fwd_f32x2_r4_j4_b3_u2_tma");
+    case 25: return make_choice<float, 3, kFwd, 4, 4, 3, true, 2, true, false, false, true, true>("fwd_f32x2_r4_j4_b3_u2_tma");
     default: return make_choice<float, 3, kFwd, 2, 4, 6, true, 2, true, false, true, true>("fwd_f32x2_r2_j4_b6_u2_tma");
   }
 }
@@ -30,7 +30,7 @@ KernelChoice<float> pick_kernel<float, 3, kAdj>(int v)
 {
   switch (v) {
     case 1: return make_choice<float, 3, kAdj, 2, 4, 3>("adj_f32_r2_j4");
-    case 25: return make_choice<float, 3, kAdj, 4, 1, 3, true, 4, false, true, false, true>("adj_f32x2_r4_aos_b3_u4");
+    case 25: return make_choice<float, 3, kAdj, 4, 1, 3, true, 4, false, true, false, true, true>("adj_f32x2_r4_aos_b3_u4");
     default: return make_choice<float, 3, kAdj, 2, 2, 5, true, 2, false, false, true, true>("adj_f32x2_r2_j2_b5_u2");
   }
 }

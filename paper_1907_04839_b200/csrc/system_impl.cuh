@@ -13,6 +13,16 @@
 
 namespace lms {
 
+inline bool thin_enabled()
+{
+  static const bool on = [] {
+    const char* e = std::getenv("LMS_THIN");  // experiment knob: 0 keeps every row tile a full tile
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
+
 namespace {
 
 inline long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
@@ -144,8 +154,17 @@ void System<T, D>::pick_kernels(bool partitioned)
   // gain exceeds the extra padding (measured on B200, scripts/gpu_thresh.py: R = 4 / R = 2 ratio 0.98-0.99 at
   // N = 8000-15 000 except 1.014 at 11 000; 1.01-1.13 below 8000).
   auto padding = [&](long long rows) { return (double)round_up((long long)cfg.n, rows) / (double)std::max(cfg.n, (size_t)1) - 1.0; };
+  // ... where a mostly padded last 512-row tile counts what it costs as a thin tile (plan_for: a quarter or half of
+  // a tile's units plus one phantom cell in nine)
+  auto padding4 = [&]() {
+    const long long bm = 4 * kThreads, tiles = ceil_div((long long)cfg.n, bm), live = (long long)cfg.n - (tiles - 1) * bm;
+    const double last = !thin_enabled() ? (double)bm : live * 4 <= bm ? bm * 0.28125 : (live * 2 <= bm ? bm * 0.5625 : (double)bm);
+    return ((double)((tiles - 1) * bm) + last) / (double)std::max(cfg.n, (size_t)1) - 1.0;
+  };
   const double gain4 = cfg.n >= 16000 ? 0.035 : 0.015;
-  const bool large = batch == 1 ? (cfg.n >= 8000 && padding(4 * kThreads) - padding(2 * kThreads) < gain4)
+  // (scripts/gpu_thin.py, B200: with the thin last tile the four-row shapes win from N ~ 10 800 on -- ratio to the
+  // two-row shapes 0.978-0.997 at N = 10 800 ... 15 400 -- and lose below 10 300: 1.005-1.027)
+  const bool large = batch == 1 ? (cfg.n >= 10500 && padding4() - padding(2 * kThreads) < gain4)
                                 : (cfg.n >= 1024 && (long long)batch * (long long)cfg.n >= 32000);
   if (variant == 0 && sizeof(T) == 4 && large) variant = 25;
   k_fwd_ = pick_kernel<T, D, kFwd>(variant);
@@ -255,13 +274,31 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   p.tiles_per_problem = std::max(row_tiles >= 0 ? row_tiles : ceil_div(n_rows, p.bm), 1);
   p.n_row_tiles = (row_tiles >= 0 ? row_tiles : ceil_div(n_rows, p.bm)) * batch_count;
   p.n_j_tiles = ceil_div((long long)cfg.n, kTileJ);
-  (void)row_tile0;
   const long long units_per_row = (long long)p.n_j_tiles * kUnitsPerTile;  // work units, see pair_kernel
-  // (Tried: letting the dead warps of a mostly-padded last row tile skip the pair math and giving that tile
-  // proportionally fewer work units.  A CTA's time is set by its busiest warp, not by how many warps work, so the
-  // "cheaper" tile just ran 4x longer per unit: N = 20 000 went from 8.1 to 16-20 ms.  Row tiles that are mostly
-  // padding cost a full tile: 2.3 % of a launch at N = 20 000 with 512-row tiles, 3.6 % with 768.)
-  const long long cells = (long long)p.n_row_tiles * units_per_row;
+  // Thin last row tile.  A row tile that is mostly padding used to cost a full tile (2.3 % of a launch at N = 20 000
+  // with 512-row tiles: 40 tiles for 39.06 tiles' worth of rows).  When its live rows fit the threads of a quarter (or
+  // half) of the CTA, those rows are replicated over 4 (2) groups of warps, each group sweeping a quarter (half) of
+  // every staged column tile, and the tile counts a quarter (half) of a tile's work units (pair_kernel, `thin`).
+  // Every warp stays busy, so -- unlike an earlier attempt that let the dead warps of that tile idle and found a
+  // CTA's time set by its busiest warp -- the tile's cost really shrinks.  Single problems on one GPU only.
+  const bool thin_on = thin_enabled();
+  const bool all_rows = row_tiles < 0 || (row_tile0 == 0 && row_tiles == ceil_div(n_rows, p.bm));
+  if (thin_on && k.thin_ok && all_rows && batch_count == 1 && !comm_active_ && !cluster_combine_ && p.n_row_tiles >= 1) {
+    const long long live_last = (long long)n_rows - (long long)(p.n_row_tiles - 1) * p.bm;
+    if (live_last * 4 <= p.bm) p.thin_split = 4;
+    else if (live_last * 2 <= p.bm) p.thin_split = 2;
+  }
+  // A thin tile's units cost a few per cent more than a full tile's (a whole column tile is staged and waited for per
+  // 1/thin_split of the work), and stream-K hands every CTA the same number of cells: one cell in `thin_period` of that
+  // tile is a phantom, so its CTAs do not finish last (measured).
+  static const int thin_period = [] {
+    const char* e = std::getenv("LMS_THIN_PERIOD");  // experiment knob: 0 = no phantom cells
+    return e ? std::max(std::atoi(e), 0) : 9;
+  }();
+  if (p.thin_split > 1 && thin_period > 1) p.thin_period = thin_period;
+  const long long thin_units = units_per_row / p.thin_split;
+  const long long thin_cells = thin_units + (p.thin_period > 1 ? thin_units / (p.thin_period - 1) : 0);
+  const long long cells = (long long)p.n_row_tiles * units_per_row - (units_per_row - thin_cells);
   if (cells <= 0) return p;
   int per_sm = 0;
   LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kThreads, 0));
@@ -393,6 +430,8 @@ PairArgs<T> System<T, D>::base_args() const
   a.n_cols = n();
   a.n_rows = n();
   a.row_tile0 = 0;
+  a.thin_split = 1;
+  a.thin_period = 0;
   a.hp0 = hp0_;
   a.target = target_;
   a.grad_out = d_grad_;
@@ -424,6 +463,8 @@ void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchP
   a.n_row_tiles = plan.n_row_tiles;
   a.tiles_per_problem = plan.tiles_per_problem;
   a.n_j_tiles = plan.n_j_tiles;
+  a.thin_split = plan.thin_split;
+  a.thin_period = plan.thin_period;
   if (plan.partial_elems > partials_cap_ || plan.grid > counters_cap_)
     throw StatusError{LMS_ERR_STATE, "launch plan outgrew the stream-K partial buffers"};
   a.partials = partials_;

@@ -222,6 +222,39 @@ def test_fp32_shape_variants_agree_with_oracle(hs, oracle, variant, n):
     assert rel_inf(da, oda) <= 1e-5 and rel_inf(db, odb) <= 1e-5
 
 
+@pytest.mark.parametrize("n", [30, 128, 129, 544, 640, 641, 768, 769, 1056, 2180])
+def test_thin_last_row_tile_agrees_with_oracle(hs, oracle, n):
+    """Four-row shapes (variant 25, the default from N = 16 000) on the tiled path: a last 512-row tile holding at most
+    128 (256) live rows is swept as a thin tile -- its rows replicated over 4 (2) groups of warps, each sweeping a
+    quarter (half) of every staged column tile, with phantom cells in the stream-K cell space.  Sizes at and around
+    both thresholds, a single thin tile, and thin tiles behind one to four full ones; every entry point that launches
+    the pair kernels, and run-to-run bitwise reproducibility."""
+    q, p, target, *_ = synth_case(n, 3, 900 + n, spread=7.0)
+    s = hs(n, 3, "f32", variant=25, tiled_only=True)
+    r = s.compute_gradient(q, p, target, 10.0, 4)
+    loss, kin, mm, grad = oracle.compute_gradient("f32", q, p, target, SIGMA, 10.0, 4)
+    assert r.loss == pytest.approx(loss, rel=1e-5) and rel_inf(r.grad, grad) <= 1e-5
+    again = s.compute_gradient(q, p, target, 10.0, 4)
+    assert np.array_equal(again.grad, r.grad) and again.loss == r.loss
+    hq, hp = s.derivatives(q, p)
+    ohq, ohp = oracle.derivatives("f32", q, p, SIGMA)
+    assert rel_inf(hq, ohq) <= 1e-5 and rel_inf(hp, ohp) <= 1e-5
+    assert s.hamiltonian(q, p) == pytest.approx(oracle.hamiltonian("f32", q, p, SIGMA), rel=1e-5)
+    alpha, beta = p[::-1].copy(), q[::-1].copy() * 0.1
+    da, db = s.adjoint_step(q, p, alpha, beta)
+    oda, odb = oracle.adjoint_step("f32", q, p, alpha, beta, SIGMA)
+    assert rel_inf(da, oda) <= 1e-5 and rel_inf(db, odb) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [544, 1200])
+def test_thin_last_row_tile_two_dimensional(hs, oracle, n):
+    q, p, target, *_ = synth_case(n, 2, 60 + n, spread=9.0)
+    s = hs(n, 2, "f32", variant=25, tiled_only=True)
+    r = s.compute_gradient(q, p, target, 10.0, 4)
+    loss, kin, mm, grad = oracle.compute_gradient("f32", q, p, target, SIGMA, 10.0, 4)
+    assert r.loss == pytest.approx(loss, rel=1e-5) and rel_inf(r.grad, grad) <= 1e-5
+
+
 @pytest.mark.parametrize("n", [700, 1500])
 def test_two_dimensional_four_row_shapes(hs, oracle, n):
     """D = 2 with the shapes large problems select (variant 25)."""
@@ -236,8 +269,10 @@ def test_default_shapes_switch_with_problem_size(hs):
     """Variant 0 chooses the kernel shapes by problem size (System::pick_kernels)."""
     r2 = b"fwd_f32x2_r2_j4_b6_u2_tma / adj_f32x2_r2_j2_b5_u2"
     r4 = b"fwd_f32x2_r4_j4_b3_u2_tma / adj_f32x2_r4_aos_b3_u4"
-    # four rows per thread from N = 8000 on, unless their 512-row tiles pad more than they gain (N = 11 000: 2.4 % vs 0.07 %)
-    for n, want in ((2000, r2), (7000, r2), (10000, r4), (11000, r2), (16000, r4), (20000, r4)):
+    # four rows per thread from N = 10 500 on, unless their 512-row tiles pad more than they gain -- a last tile that is
+    # at most half live rows counts as the thin tile it is swept as (N = 11 000: 0.36 % vs 0.07 %; N = 12 200: last tile
+    # 424 live rows of 512, 0.7 % more padding than 256-row tiles, still within the 1.5 % the shapes gain)
+    for n, want in ((2000, r2), (7000, r2), (10000, r2), (11000, r4), (12200, r4), (16000, r4), (20000, r4)):
         s = hs(n, 3, "f32")
         assert s.lib.lms_system_kernel_names(s.handle) == want, n
 
