@@ -127,7 +127,9 @@ struct KernelChoice {
   void (*fn_cluster)(PairArgs<T>) = nullptr;  // same shape with the cluster combine (small problems), or null
   void (*fn_peers)(PairArgs<T>) = nullptr;    // same shape with the peer-push stores in its epilogues (row partition), or null
   int rows_per_thread = 0;
-  bool thin_ok = false;  // fn carries the thin-last-row-tile code (PairArgs::thin_split)
+  void (*fn_thin)(PairArgs<T>) = nullptr;     // same shape with the thin-last-row-tile code (PairArgs::thin_split), or null:
+                                              // launched only when the plan has a thin tile, so launches without one
+                                              // (other sizes, batches, row partitions) run the kernel they always ran
   const char* name = "";
 };
 
@@ -136,8 +138,8 @@ template <typename T, int D, int MODE, int R, int JU, int MINB, bool PACKED = fa
 KernelChoice<T> make_choice(const char* name)
 {
   KernelChoice<T> c;
-  c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, false, false, WITH_THIN>;
-  c.thin_ok = WITH_THIN;
+  c.fn = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS>;
+  if constexpr (WITH_THIN) c.fn_thin = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, false, false, true>;
   if constexpr (WITH_CLUSTER) c.fn_cluster = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, true>;
   if constexpr (WITH_PEERS) c.fn_peers = pair_kernel<T, D, MODE, R, JU, MINB, PACKED, UNR, BULK, AOS, false, true>;
   c.rows_per_thread = R;

@@ -153,19 +153,21 @@ void System<T, D>::pick_kernels(bool partitioned)
   // 512-row tiles pad more (N = 11 000: 2.4 % against 0.07 % for 256-row tiles).  Padding-aware: take them when the
   // gain exceeds the extra padding (measured on B200, scripts/gpu_thresh.py: R = 4 / R = 2 ratio 0.98-0.99 at
   // N = 8000-15 000 except 1.014 at 11 000; 1.01-1.13 below 8000).
-  auto padding = [&](long long rows) { return (double)round_up((long long)cfg.n, rows) / (double)std::max(cfg.n, (size_t)1) - 1.0; };
-  // ... where a mostly padded last 512-row tile counts what it costs as a thin tile (plan_for: a quarter or half of
-  // a tile's units plus one phantom cell in nine)
-  auto padding4 = [&]() {
-    const long long bm = 4 * kThreads, tiles = ceil_div((long long)cfg.n, bm), live = (long long)cfg.n - (tiles - 1) * bm;
-    const double last = !thin_enabled() ? (double)bm : live * 4 <= bm ? bm * 0.28125 : (live * 2 <= bm ? bm * 0.5625 : (double)bm);
+  // Padding of the last row tile, counted as what it costs: a mostly padded tile is swept as a thin tile (plan_for: a
+  // quarter or half of a tile's units plus one phantom cell in nine) by the shapes that have that instantiation.
+  auto padding = [&](long long bm, bool thin) {
+    const long long tiles = ceil_div((long long)cfg.n, bm), live = (long long)cfg.n - (tiles - 1) * bm;
+    const double last = !(thin && thin_enabled()) ? (double)bm
+                        : live * 4 <= bm ? bm * 0.28125 : (live * 2 <= bm ? bm * 0.5625 : (double)bm);
     return ((double)((tiles - 1) * bm) + last) / (double)std::max(cfg.n, (size_t)1) - 1.0;
   };
+  const bool thin2 = pick_kernel<T, D, kFwd>(0).fn_thin != nullptr, thin4 = pick_kernel<T, D, kFwd>(25).fn_thin != nullptr;
   const double gain4 = cfg.n >= 16000 ? 0.035 : 0.015;
   // (scripts/gpu_thin.py, B200: with the thin last tile the four-row shapes win from N ~ 10 800 on -- ratio to the
   // two-row shapes 0.978-0.997 at N = 10 800 ... 15 400 -- and lose below 10 300: 1.005-1.027)
-  const bool large = batch == 1 ? (cfg.n >= 10500 && padding4() - padding(2 * kThreads) < gain4)
-                                : (cfg.n >= 1024 && (long long)batch * (long long)cfg.n >= 32000);
+  bool large = batch == 1 ? (cfg.n >= 10500 && padding(4 * kThreads, thin4) - padding(2 * kThreads, thin2) < gain4)
+                          : (cfg.n >= 1024 && (long long)batch * (long long)cfg.n >= 32000);
+  if (const char* e = std::getenv("LMS_FORCE_ROWS")) large = std::atoi(e) == 4;  // experiment knob: 2 or 4 rows per thread
   if (variant == 0 && sizeof(T) == 4 && large) variant = 25;
   k_fwd_ = pick_kernel<T, D, kFwd>(variant);
   k_adj_ = pick_kernel<T, D, kAdj>(variant);
@@ -283,7 +285,7 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   // CTA's time set by its busiest warp -- the tile's cost really shrinks.  Single problems on one GPU only.
   const bool thin_on = thin_enabled();
   const bool all_rows = row_tiles < 0 || (row_tile0 == 0 && row_tiles == ceil_div(n_rows, p.bm));
-  if (thin_on && k.thin_ok && all_rows && batch_count == 1 && !comm_active_ && !cluster_combine_ && p.n_row_tiles >= 1) {
+  if (thin_on && k.fn_thin != nullptr && all_rows && batch_count == 1 && !comm_active_ && !cluster_combine_ && p.n_row_tiles >= 1) {
     const long long live_last = (long long)n_rows - (long long)(p.n_row_tiles - 1) * p.bm;
     if (live_last * 4 <= p.bm) p.thin_split = 4;
     else if (live_last * 2 <= p.bm) p.thin_split = 2;
@@ -300,8 +302,9 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   const long long thin_cells = thin_units + (p.thin_period > 1 ? thin_units / (p.thin_period - 1) : 0);
   const long long cells = (long long)p.n_row_tiles * units_per_row - (units_per_row - thin_cells);
   if (cells <= 0) return p;
+  const auto fn_launched = p.thin_split > 1 ? k.fn_thin : k.fn;  // see launch()
   int per_sm = 0;
-  LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kThreads, 0));
+  LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn_launched, kThreads, 0));
   per_sm = std::max(per_sm, 1);
   static const int cap_per_sm = [] {
     const char* e = std::getenv("LMS_CTAS_PER_SM");  // experiment knob: cap on resident CTAs per SM
@@ -371,7 +374,7 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   }();
   if (combine_smem_on && !p.cluster && !comm_active_ && batch_count == 1 && p.grid <= 2 * num_sms_ && p.n_row_tiles >= 1) {
     cudaFuncAttributes attr;
-    LMS_CUDA(cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(k.fn)));
+    LMS_CUDA(cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(fn_launched)));
     const size_t seg_bytes = (size_t)NA * p.bm * sizeof(T);
     const size_t per_sm = 227 * 1024;
     const long long budget = (long long)(per_sm / 2) - (long long)attr.sharedSizeBytes - 2048;  // two CTAs per SM
@@ -381,9 +384,9 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
     if (segs > kCombineUnroll) {  // otherwise the register path moves as many segments per round trip
       int occ = 0;
       const size_t dyn = (size_t)segs * seg_bytes;
-      LMS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k.fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+      LMS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn_launched), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)dyn));
-      LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, kThreads, dyn));
+      LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn_launched, kThreads, dyn));
       if ((long long)occ * num_sms_ >= p.grid) {
         p.combine_segments = segs;
         p.dyn_smem = dyn;
@@ -407,6 +410,11 @@ void System<T, D>::alloc_partials()
   auto account = [&](const KernelChoice<T>& k, int na) {
     int per_sm = 0;
     LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kThreads, 0));
+    if (k.fn_thin != nullptr) {
+      int per_sm_thin = 0;
+      LMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_thin, k.fn_thin, kThreads, 0));
+      per_sm = std::max(per_sm, per_sm_thin);
+    }
     const int full = num_sms_ * std::max(per_sm, 1);
     grid_max = std::max(grid_max, full);
     elems = std::max(elems, (size_t)2 * full * na * kThreads * k.rows_per_thread);
@@ -471,7 +479,7 @@ void System<T, D>::launch(const KernelChoice<T>& k, PairArgs<T> a, const LaunchP
   a.counters = counters_;
   a.combine_smem_segments = plan.combine_segments;
   // the peer-push stores exist only in the PEERS instantiation of a shape (pair_kernels.cuh, put_all)
-  auto fn = k.fn;
+  auto fn = plan.thin_split > 1 ? k.fn_thin : k.fn;
   if (a.n_peers > 0) {
     if (k.fn_peers == nullptr)
       throw StatusError{LMS_ERR_STATE, "this kernel variant has no peer-push instantiation (use the default variant)"};

@@ -43,6 +43,12 @@ for prec in ("f32", "f64"):
     q5 = rng.uniform(-14, 14, (n5, 3)); p5 = rng.normal(size=(n5, 3)); t5k = q5 + 0.3 * rng.normal(size=(n5, 3))
     s = HamiltonianSystem(1.5, n5, 3, prec, max_timesteps=2, tiled_only=True)
     print("mid-size", s.compute_gradient(q5, p5, t5k, 10.0, 2).loss, s.last_eval_kernel_launches()); s.close()
+    # the thin last row tile of the four-row shapes (variant 25): 4 and 2 column groups, alone and behind full tiles
+    for nt in (30, 544, 700, 1056):
+        qt = rng.uniform(-8, 8, (nt, 3)); pt = rng.normal(size=(nt, 3)); tt = qt + 0.3 * rng.normal(size=(nt, 3))
+        s = HamiltonianSystem(1.5, nt, 3, prec, max_timesteps=2, variant=25, tiled_only=True)
+        print("thin tile", nt, s.compute_gradient(qt, pt, tt, 10.0, 2).loss, s.last_eval_kernel_launches())
+        s.derivatives(qt, pt); s.close()
     # (the in-process peer-push test is left out: compute-sanitizer serialises kernel launches of the process, so
     #  a rank's stream-ordered wait for its peer's flag blocks the very launch that would set it)
     s = HamiltonianSystem(1.5, n, 3, prec, max_timesteps=T)

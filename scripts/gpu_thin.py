@@ -1,8 +1,7 @@
-"""Thin last row tile (PairArgs::thin_split): device ms per gradient, T = 10, fp32, for
-  A  variant 0 with LMS_THIN=0  (the size rule without the thin tile: two- or four-row shapes as before)
-  B  variant 25 (four-row shapes), LMS_THIN=0
-  C  variant 25, thin tile on (default phantom period)
-  D  variant 0, thin tile on (what ships)
+"""Thin last row tile (PairArgs::thin_split): device ms per gradient on the tiled path, T = 10, fp32, for
+  R2 / R2t   two-row shapes (LMS_FORCE_ROWS=2) without / with the thin tile
+  R4 / R4t   four-row shapes (LMS_FORCE_ROWS=4) without / with the thin tile
+  ships      what the size rule of pick_kernels chooses (thin tile on)
 usage: python scripts/gpu_thin.py N [N ...]"""
 import json
 import os
@@ -31,11 +30,12 @@ if sys.argv[1] == "child":
     sys.exit(0)
 for n in [int(a) for a in sys.argv[1:]]:
     row = {}
-    for name, v, env in (("A", 0, {"LMS_THIN": "0"}), ("B", 25, {"LMS_THIN": "0"}), ("C", 25, {}), ("D", 0, {})):
-        out = subprocess.run([sys.executable, __file__, "child", str(n), str(v)], env=dict(os.environ, **env),
+    for name, env in (("R2", {"LMS_FORCE_ROWS": "2", "LMS_THIN": "0"}), ("R2t", {"LMS_FORCE_ROWS": "2"}),
+                      ("R4", {"LMS_FORCE_ROWS": "4", "LMS_THIN": "0"}), ("R4t", {"LMS_FORCE_ROWS": "4"}), ("ships", {})):
+        out = subprocess.run([sys.executable, __file__, "child", str(n), "0"], env=dict(os.environ, **env),
                              capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
         row[name] = json.loads(out)
-    r4 = "r4" in row["A"]["kernels"]
-    print(f"N={n:6d}  A(old rule: {'R4' if r4 else 'R2'}) {row['A']['ms']:7.3f}  B(R4) {row['B']['ms']:7.3f}  "
-          f"C(R4 thin) {row['C']['ms']:7.3f}  D(ships: {'R4' if 'r4' in row['D']['kernels'] else 'R2'}) {row['D']['ms']:7.3f}  "
-          f"C/B {row['C']['ms'] / row['B']['ms']:.4f}  D/A {row['D']['ms'] / row['A']['ms']:.4f}", flush=True)
+    best = min(("R2t", "R4t"), key=lambda k: row[k]["ms"])
+    print(f"N={n:6d}  R2 {row['R2']['ms']:7.3f}  R2t {row['R2t']['ms']:7.3f}  R4 {row['R4']['ms']:7.3f}  R4t {row['R4t']['ms']:7.3f}  "
+          f"ships {'R4' if 'r4' in row['ships']['kernels'] else 'R2'} {row['ships']['ms']:7.3f}  best {best}  "
+          f"ships/best {row['ships']['ms'] / row[best]['ms']:.4f}", flush=True)
