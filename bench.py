@@ -510,8 +510,11 @@ def b200_arm(args):
             "forward_kernel": {"avg_launch_ms": fwd_ms, "achieved": fwd_rate / 1e12, "frac": fwd_rate / peak_slots,
                                "algorithmic_slots_per_pair": f_slots, "executed_slots_per_pair": f_exec,
                                "frac_executed": f_exec * pairs_per_launch / (fwd_ms * 1e-3) / peak_slots},
+            # `frac`: from the separately timed launches of the pass above (events around every launch, no graph);
+            # `frac_of_timed_step`: the same slots over the headline step time (one graph launch per gradient)
             "gradient": {"achieved": grad_rate / 1e12, "frac": grad_rate / peak_slots,
-                         "slots_per_gradient": (f_slots + a_slots) * T * pairs_per_launch},
+                         "slots_per_gradient": (f_slots + a_slots) * T * pairs_per_launch,
+                         "frac_of_timed_step": (f_slots + a_slots) * T * pairs_per_launch / (dev_ms / K * 1e-3) / peak_slots},
             "hbm": {"algorithmic_bytes_per_launch": bytes_per_launch,
                     "achieved_gbs": bytes_per_launch / (adj_ms * 1e-3) / 1e9, "peak_gbs": peaks.get("hbm_gbs")},
             "kernel_share_of_step": (fwd_ms + adj_ms) * T / (dev_ms / K),
