@@ -11,7 +11,7 @@ T = 10
 bad = 0
 for n, prec, r in ((257, "f32", reps), (1000, "f32", reps), (1000, "f64", reps), (3000, "f32", reps), (4096, "f32", reps // 3),
                    (2048, "f64", reps // 3), (3400, "f64", reps // 6), (5000, "f32", reps // 3), (8192, "f32", reps // 6),
-                   (9000, "f32", reps // 6), (20000, "f32", reps // 30)):
+                   (9000, "f32", reps // 6), (12400, "f32", reps // 10), (20000, "f32", reps // 15)):  # 9000 ... 20000: thin last row tile
     q0 = make_template_points(n, 40.0 * float(np.sqrt(n / 1847.0)))
     target = q0 + 0.5 * rng_normals(1, n * 3).reshape(n, 3)
     x0 = np.ascontiguousarray(((target - q0) / T).ravel())
