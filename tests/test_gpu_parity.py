@@ -786,6 +786,57 @@ def test_large_n_row_subset_fp32(oracle):
     s.close()
 
 
+def test_configs2_full_size_properties_fp32(oracle):
+    """BASELINE configs[2] on one GPU -- N = 200 000, T = 20, fp32, the evaluation bench.py times at that size -- through
+    the properties that do not need an O(N^2) CPU run: momentum conservation of the Euler flow over
+    all 21 snapshots, H = 1/2 sum p.hp and sum_i hq_i = 0, "at the true momenta of a reachable target the gradient is
+    hp(q0, p) and the loss is H" (the fp64 flow of the same handle family builds the target), a directional finite
+    difference of the loss at the paper's initial point, and 40 rows of the final positions against the oracle's own
+    per-row sums for the first Euler step."""
+    from paper_1907_04839_b200 import HamiltonianSystem, make_synthetic_pair
+
+    n, T, lam = 200000, 20, 5e5
+    q0, target, p_true = make_synthetic_pair(n, SIGMA, T, density_scaled=True)
+    s = HamiltonianSystem(SIGMA, n, 3, "f32", max_timesteps=T)
+    tq, tp = s.integrate_forward(q0, p_true, T)
+    # fp32 flow against the fp64 flow that made the target
+    assert rel_inf(tq[-1], target) <= 1e-5
+    drift = np.abs(tp.sum(axis=1) - p_true.sum(axis=0)).max()
+    assert drift <= 1e-5 * np.linalg.norm(p_true, axis=1).sum() / np.sqrt(n)  # N random roundings of ~6e-8 |p| each
+    # first Euler step of 40 rows against the oracle's per-row sums: q1 = q0 + dt hp, p1 = p0 - dt hq
+    rows = np.unique(np.concatenate([[0, 511, 512, n - 1], np.random.default_rng(2).integers(0, n, 36)]))
+    ohq, ohp = oracle.pair_rows("f32", q0, p_true, rows, SIGMA)
+    dt = 1.0 / T
+    assert np.abs(tq[1][rows] - (q0[rows] + dt * ohp)).max() <= 1e-5 * np.abs(tq[1]).max()
+    assert np.abs(tp[1][rows] - (p_true[rows] - dt * ohq)).max() <= 1e-5 * np.abs(tp[1]).max()
+    del tq, tp
+    h = s.hamiltonian(q0, p_true)
+    hq, hp = s.derivatives(q0, p_true)
+    assert 0.5 * float((p_true * hp).sum()) == pytest.approx(h, rel=1e-6)
+    assert np.abs(hq.sum(axis=0)).max() <= 1e-5 * np.abs(hq).sum() / np.sqrt(n)
+    # the fp32 flow misses the fp64 target by rounding only: loss = H + lambda * (rounding)^2, grad = hp + 2 lambda * rounding
+    s.bind_registration(q0, target, lam, T)
+    loss, grad = s.objective(p_true)
+    assert s.last_kinetic == pytest.approx(h, rel=1e-6)
+    assert s.last_mismatch <= n * 3 * (1e-5 * np.abs(target).max()) ** 2
+    assert s.last_eval_kernel_launches() == 2 * T + 2
+    # finite difference of the loss along its own gradient at the paper's initial point (registration.cpp:47-52).  The
+    # fp32 loss (~1e11 here) carries ~1e-7 of relative rounding noise, which swamps the slope along a random unit vector
+    # (~|g| / sqrt(3N)); along g / |g| the slope is |g| itself and a central difference resolves it to about a per cent.
+    x0 = np.ascontiguousarray(((target - q0) / T).ravel())
+    loss0, g0 = s.objective(x0)
+    again, g1 = s.objective(x0)
+    assert again == loss0 and np.array_equal(g0, g1)  # bitwise run to run at this size too
+    gnorm = float(np.linalg.norm(g0))
+    v = g0 / gnorm
+    eps = 3e-2
+    hi, _ = s.objective(x0 + eps * v)
+    lo, _ = s.objective(x0 - eps * v)
+    assert hi > loss0 > lo
+    assert (hi - lo) / (2 * eps) == pytest.approx(gnorm, rel=2e-2)
+    s.close()
+
+
 @pytest.mark.parametrize("prec", ["f32", "f64"])
 @pytest.mark.parametrize("world,n", [(2, 1500), (3, 2600), (4, 700), (2, 20000)])
 def test_row_partition_loopback(hs, oracle, prec, world, n):
