@@ -20,7 +20,9 @@ namespace lms {
 // Shapes measured in round 1 and dropped from the build (numbers per launch at N = 20 000, one session, ms):
 //   forward R=4: j4 0.2584 | j2_u2 0.2508 | j4_u2 0.2500 | j4_u2_tma 0.2468 (kept) | j4_u4 0.2554 | j2_u4 0.2589;
 //   adjoint R=4: aos_u4 0.5536 (kept) | aos_u2 0.5660 | j4_tma 0.5558 | j2_u2_tma 0.5633 | j2_tma 0.5661;
-//   R=6 / R=8: 0.8 % faster per pair, lost to row-tile quantisation.
+//   R=6 / R=8: 0.8 % faster per pair, lost to row-tile quantisation.  Round 2, R=6 again with the current
+//   loops (forward u2 + TMA at 246 registers, adjoint column-major u4 at 240, 2 CTAs/SM) and the thin last tile, ms per
+//   gradient R=4 / R=6: N = 20 000 7.841 / 7.950, 50 000 47.29 / 47.54, 100 000 188.4 / 188.9 -- no longer ahead.
 template <>
 KernelChoice<float> pick_kernel<float, 3, kFwd>(int v)
 {
