@@ -149,10 +149,10 @@ void System<T, D>::pick_kernels(bool partitioned)
 {
   int variant = cfg.variant;
   // (populations: the same shapes once the batch as a whole is that large -- 128 x N = 2000: 10.81 -> 10.49 ms)
-  // Single problems: four rows per thread are 1-2 % faster per gradient from N = 8000 on and 3-4 % from 16 000 on, but their
+  // Single problems: four rows per thread are 1-2 % faster per gradient from N ~ 10 500 on and 3-4 % from 16 000 on, but their
   // 512-row tiles pad more (N = 11 000: 2.4 % against 0.07 % for 256-row tiles).  Padding-aware: take them when the
   // gain exceeds the extra padding (measured on B200, scripts/gpu_thresh.py: R = 4 / R = 2 ratio 0.98-0.99 at
-  // N = 8000-15 000 except 1.014 at 11 000; 1.01-1.13 below 8000).
+  // N = 8000-15 000 except 1.014 at 11 000; 1.01-1.13 below 8000 -- before the thin last tile; with it see below).
   // Padding of the last row tile, counted as what it costs: a mostly padded tile is swept as a thin tile (plan_for: a
   // quarter or half of a tile's units plus one phantom cell in nine) by the shapes that have that instantiation.
   auto padding = [&](long long bm, bool thin) {

@@ -9,16 +9,16 @@ SO = "paper_1907_04839_b200/liblmshoot_b200.so"
 tag = sys.argv[1] if len(sys.argv) > 1 else "r2"
 # (title, demangled-name substring, executed FP-pipe lane-ops per pair the roofline section relies on)
 KERNELS = [
-    ("fp32 forward, N >= 8000 (`fwd_f32x2_r4_j4_b3_u2_tma`)", "pair_kernel<float, 3, 0, 4, 4, 3, true, 2, true, false, false, false, false>", "17 + 1 ex2"),
-    ("fp32 adjoint, N >= 8000 (`adj_f32x2_r4_aos_b3_u4`)", "pair_kernel<float, 3, 1, 4, 1, 3, true, 4, false, true, false, false, false>", "39 + 1 ex2"),
+    ("fp32 forward, four rows (N >= 10 500 unless padding says otherwise), full-tile instantiation (`fwd_f32x2_r4_j4_b3_u2_tma`)", "pair_kernel<float, 3, 0, 4, 4, 3, true, 2, true, false, false, false, false>", "17 + 1 ex2"),
+    ("fp32 adjoint, four rows (N >= 10 500 unless padding says otherwise), full-tile instantiation (`adj_f32x2_r4_aos_b3_u4`)", "pair_kernel<float, 3, 1, 4, 1, 3, true, 4, false, true, false, false, false>", "39 + 1 ex2"),
     ("fp32 forward, four rows, thin-tile instantiation: what a launch with a thin last row tile runs, e.g. N = 20 000 (`fwd_f32x2_r4_j4_b3_u2_tma`; the full-tile sweep is the loop below, the thin-tile sweep a second copy)", "pair_kernel<float, 3, 0, 4, 4, 3, true, 2, true, false, false, false, true>", "17 + 1 ex2"),
     ("fp32 adjoint, four rows, thin-tile instantiation (N = 20 000)", "pair_kernel<float, 3, 1, 4, 1, 3, true, 4, false, true, false, false, true>", "39 + 1 ex2"),
-    ("fp32 forward, N < 8000 (`fwd_f32x2_r2_j4_b6_u2_tma`)", "pair_kernel<float, 3, 0, 2, 4, 6, true, 2, true, false, false, false, false>", "17 + 1 ex2"),
-    ("fp32 adjoint, N < 8000 (`adj_f32x2_r2_j2_b5_u2`)", "pair_kernel<float, 3, 1, 2, 2, 5, true, 2, false, false, false, false, false>", "39 + 1 ex2"),
+    ("fp32 forward, two rows (N < 10 500) (`fwd_f32x2_r2_j4_b6_u2_tma`)", "pair_kernel<float, 3, 0, 2, 4, 6, true, 2, true, false, false, false, false>", "17 + 1 ex2"),
+    ("fp32 adjoint, two rows (N < 10 500) (`adj_f32x2_r2_j2_b5_u2`)", "pair_kernel<float, 3, 1, 2, 2, 5, true, 2, false, false, false, false, false>", "39 + 1 ex2"),
     ("fp64 forward (`fwd_f64_r2_j2_u2_tma`)", "pair_kernel<double, 3, 0, 2, 2, 3, false, 2, true, false, false, false, false>", "28"),
     ("fp64 adjoint (`adj_f64_r2_j2_u2_tma`)", "pair_kernel<double, 3, 1, 2, 2, 2, false, 2, true, false, false, false, false>", "50"),
     ("persistent small-N kernel, fp32, single-window instantiation (`small_eval_kernel<float,3,1,2>`)", "small_eval_kernel<float, 3, 1, 2>", "17 + 1 / 39 + 1"),
-    ("fp32 adjoint, N >= 8000, peer-push instantiation (row partition only)", "pair_kernel<float, 3, 1, 4, 1, 3, true, 4, false, true, false, true, false>", "39 + 1 ex2"),
+    ("fp32 adjoint, four rows (N >= 10 500 unless padding says otherwise), full-tile instantiation, peer-push instantiation (row partition only)", "pair_kernel<float, 3, 1, 4, 1, 3, true, 4, false, true, false, true, false>", "39 + 1 ex2"),
 ]
 sass = subprocess.run(["cuobjdump", "-sass", SO], capture_output=True, text=True, check=True).stdout
 blocks = sass.split("Function : ")[1:]
