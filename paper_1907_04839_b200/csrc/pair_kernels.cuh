@@ -33,6 +33,14 @@
 
 namespace lms {
 
+// -DLMS_TAIL_TRACE: thread 0 of every CTA that finishes a shared row tile prints the cycle counts of its hand-over
+// chain (measurement build only: scripts/gpu_tail_trace.py)
+#ifdef LMS_TAIL_TRACE
+#define LMS_TT(i) do { if (threadIdx.x == 0) tt[i] = clock64(); } while (0)
+#else
+#define LMS_TT(i) do { } while (0)
+#endif
+
 constexpr int kCombineUnroll = LMS_COMBINE_UNROLL;
 constexpr int kThreads = 128;  // threads per CTA
 constexpr int kTileJ = 128;    // columns staged per shared-memory tile
@@ -804,6 +812,10 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       }
     }
 
+#ifdef LMS_TAIL_TRACE
+    long long tt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+    LMS_TT(0);  // sweep done
     // ---- combine partial sums across the CTAs that share this row tile ----------------------------
     // (recomputed here rather than kept in registers across the sweep)
     const int grp_threads = thin ? kThreads / split : kThreads;   // threads that hold distinct rows
@@ -871,7 +883,9 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int k = 0; k < NA; ++k) __stcg(mine + k * BM + r * kThreads + tid, acc[r][k]);
+      LMS_TT(1);  // partial stores issued
       __threadfence();
+      LMS_TT(2);  // fence done
       __syncthreads();
       const int nseg = (int)(cta_last - cta_first + 1);
       // one arrival counter per shared row tile, indexed by its first CTA (unique: a CTA that covers the first
@@ -885,6 +899,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       }
       __syncthreads();
       do_epilogue = s_last != 0;
+      LMS_TT(3);  // arrival known
       if (do_epilogue) {
         __threadfence();
 #pragma unroll
@@ -939,6 +954,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       }
     }
 
+    LMS_TT(4);  // segments added
     // ---- epilogue ----------------------------------------------------------------------------
     if (do_epilogue) {
       double hsum = 0.0, msum = 0.0;
@@ -1046,6 +1062,13 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
         }
       }
     }
+#ifdef LMS_TAIL_TRACE
+    __syncthreads();
+    LMS_TT(5);  // epilogue done
+    if (threadIdx.x == 0 && do_epilogue && cta_first != cta_last)
+      printf("TT mode %d step %d cta %d rt %d nseg %d : stores %lld fence %lld arrive %lld combine %lld epilogue %lld\n", MODE, a.step,
+             (int)blockIdx.x, (int)rt_local, (int)(cta_last - cta_first + 1), tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4]);
+#endif
     c += tc1 - tc0;
   }
 }
