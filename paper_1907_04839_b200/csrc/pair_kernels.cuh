@@ -590,6 +590,11 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
   const long long nJ = (long long)a.n_j_tiles * kUnitsPerTile;
   // (THINOK: only the shapes instantiated with the thin-tile code take it; the others compile as if it did not exist)
   const int split = THINOK && a.thin_split > 1 ? a.thin_split : 1;  // > 1: the last row tile is thin and holds fewer units
+  // split == 8 (four-row packed shapes): 4 groups of warps, and inside a group the thread's two packed row pairs hold
+  // the SAME two rows and sweep the two halves of the group's column window (`pair split`)
+  constexpr bool kPairSplit = THINOK && PACKED && R == 4;
+  const bool pair_split = kPairSplit && split == 8;
+  const int groups = pair_split ? 4 : split;
   const int period = split > 1 && a.thin_period > 1 ? a.thin_period : 0;
   const long long nJ_thin = nJ / split + (period ? (nJ / split) / (period - 1) : 0);  // cells of the thin tile
   const long long cells = (long long)a.n_row_tiles * nJ - (nJ - nJ_thin);
@@ -640,8 +645,9 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     T ri[R][NR];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int grp_threads = thin ? kThreads / split : kThreads;  // threads that hold distinct rows
-      const long long row = thin ? row_of<R, PACKED>(rt, r, tid % grp_threads, grp_threads) : row_of<R, PACKED>(rt, r, tid);
+      const int grp_threads = thin ? kThreads / groups : kThreads;  // threads that hold distinct rows
+      const long long row = thin ? row_of<R, PACKED>(rt, pair_split ? (r & 1) : r, tid % grp_threads, grp_threads)
+                                 : row_of<R, PACKED>(rt, r, tid);
 #pragma unroll
       for (int k = 0; k < NR; ++k) {
         if constexpr (MODE == kAdj) {
@@ -715,7 +721,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     const int u1 = THIN ? units_of(tc1) : 0;
     const int jt0 = THIN ? u0 / upt_s : col0 / kTileJ;
     const int jt1 = THIN ? (u1 > u0 ? (u1 + upt_s - 1) / upt_s : jt0) : (col1 + kTileJ - 1) / kTileJ;
-    const int jj_base = THIN ? (tid / (kThreads / split)) * (kTileJ / split) : 0;  // this group's window of a tile
+    const int jj_base = THIN ? (tid / (kThreads / groups)) * (kTileJ / groups) : 0;  // this group's window of a tile
+    const int pair_off = THIN && pair_split ? kTileJ / 8 : 0;  // second row pair: the other half of the window
     for (int jt = jt0; jt < jt1; ++jt) {
       const bool more = jt + 1 < jt1;
       if constexpr (BULK) {
@@ -756,6 +763,27 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
             for (int u = 0; u < JU; ++u) cj[u][k] = v[u];
           }
         }
+        // thin tile of the four-row packed shapes: the second row pair reads its own columns (pair_off further on; the
+        // same ones when the tile is not pair-split)
+        constexpr bool kSecond = THIN && kPairSplit;
+        T cjb[kSecond ? JU : 1][kSecond ? NC : 1];
+        if constexpr (kSecond) {
+          if constexpr (AOS) {
+#pragma unroll
+            for (int k = 0; k < NC; k += 4) {
+              const float4 t4 = *reinterpret_cast<const float4*>(&tile[buf][jj + pair_off][k]);
+              cjb[0][k] = t4.x; cjb[0][k + 1] = t4.y; cjb[0][k + 2] = t4.z; cjb[0][k + 3] = t4.w;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+              T v[JU];
+              ColVec<T, JU>::load(&tile[buf][k][jj + pair_off], v);
+#pragma unroll
+              for (int u = 0; u < JU; ++u) cjb[u][k] = v[u];
+            }
+          }
+        }
         if constexpr (!PACKED) {
 #pragma unroll
           for (int u = 0; u < JU; ++u)
@@ -769,8 +797,16 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
             float2 cj2[NC];
 #pragma unroll
             for (int k = 0; k < NC; ++k) cj2[k] = splat2((float)cj[u][k]);
+            if constexpr (kSecond) {
+              float2 cjb2[NC];
 #pragma unroll
-            for (int rp = 0; rp < RP; ++rp) pair_term_packed<D, MODE>(ri2[rp], cj2, acc2[rp], kexp2, ns2, neg1);
+              for (int k = 0; k < NC; ++k) cjb2[k] = splat2((float)cjb[u][k]);
+              pair_term_packed<D, MODE>(ri2[0], cj2, acc2[0], kexp2, ns2, neg1);
+              pair_term_packed<D, MODE>(ri2[1], cjb2, acc2[1], kexp2, ns2, neg1);
+            } else {
+#pragma unroll
+              for (int rp = 0; rp < RP; ++rp) pair_term_packed<D, MODE>(ri2[rp], cj2, acc2[rp], kexp2, ns2, neg1);
+            }
           }
         }
       }
@@ -818,9 +854,21 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
     LMS_TT(0);  // sweep done
     // ---- combine partial sums across the CTAs that share this row tile ----------------------------
     // (recomputed here rather than kept in registers across the sweep)
-    const int grp_threads = thin ? kThreads / split : kThreads;   // threads that hold distinct rows
+    const int grp_threads = thin ? kThreads / groups : kThreads;  // threads that hold distinct rows
     const int grp = thin ? tid / grp_threads : 0;                 // column group of this thread (warp-uniform)
     const int gtid = tid - grp * grp_threads;                     // its index within the group
+    if constexpr (kPairSplit) {
+      if (thin && pair_split) {
+        // both row pairs hold sums of the same two rows over the two halves of the window: first half + second half
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+          acc[0][k] += acc[2][k];
+          acc[1][k] += acc[3][k];
+          acc[2][k] = T(0);
+          acc[3][k] = T(0);
+        }
+      }
+    }
     if (thin) {
       // the `split` column groups hold partial sums of the same rows: group 0 adds them in ascending group
       // (= ascending column-within-tile) order, one accumulator at a time through the reduction scratch
@@ -833,7 +881,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
           __syncthreads();
           if (grp == 0) {
             T v = acc[r][k];
-            for (int g = 1; g < split; ++g) v += red[g * grp_threads + gtid];
+            for (int g = 1; g < groups; ++g) v += red[g * grp_threads + gtid];
             acc[r][k] = v;
           }
           __syncthreads();
@@ -960,8 +1008,9 @@ __global__ void __launch_bounds__(kThreads, MINB) pair_kernel(const PairArgs<T> 
       double hsum = 0.0, msum = 0.0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const long long row = row_of<R, PACKED>(rt, r, gtid, grp_threads);
-        const bool live = row < a.n_rows && grp == 0;  // thin tile: group 0 holds the sums
+        const bool second_pair = thin && pair_split && r >= 2;  // pair-split thin tile: rows live in the first pair only
+        const long long row = row_of<R, PACKED>(rt, second_pair ? (r & 1) : r, gtid, grp_threads);
+        const bool live = row < a.n_rows && grp == 0 && !second_pair;  // thin tile: group 0 holds the sums
         if constexpr (MODE == kVel) {
           if (live) {
             if (a.epi & kEpiEuler) {

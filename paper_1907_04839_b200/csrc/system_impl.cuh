@@ -13,6 +13,28 @@
 
 namespace lms {
 
+// Phantom-cell period of a thin tile (one cell in `period` sweeps nothing), by kernel mode and split: the cost of a
+// thin cell over a full one is the per-staged-tile overhead spread over 1/split of the work, larger for the forward
+// kernel (TMA-staged tiles, 8 columns per unrolled iteration) than for the adjoint (measured: DESIGN.md §3).
+// Measured at N = 20 000 (ms per launch; full table in DESIGN.md §3): forward, 4 groups, period 9 / 7 / 5 / 4 / 3: 0.2464 /
+// 0.2450 / 0.2428 / 0.2429 / 0.2456; adjoint, 4 groups, none / 13 / 9 / 5: 0.5555 / 0.5436 / 0.5439 / 0.5445; adjoint swept
+// 8 ways, period 9 / 5 / 3 / 2: 0.5452 / 0.5425 / 0.5437 / 0.5436; forward swept 8 ways, period 2: 0.2429 (no better than 4).
+inline int thin_period_default(int mode, int split)
+{
+  if (mode == kFwd) return split >= 8 ? 2 : 5;
+  return split >= 8 ? 5 : 9;
+}
+
+// Sweeping a thin tile 8 ways (pair split) pays in the adjoint kernel only (see the table above).
+inline bool thin8_enabled(int mode)
+{
+  static const int knob = [] {
+    const char* e = std::getenv("LMS_THIN8");  // experiment knob: 0 = at most 4 ways, 1 = forward and adjoint
+    return e ? std::atoi(e) : -1;
+  }();
+  return knob >= 0 ? knob != 0 : mode == kAdj;
+}
+
 inline bool thin_enabled()
 {
   static const bool on = [] {
@@ -158,6 +180,7 @@ void System<T, D>::pick_kernels(bool partitioned)
   auto padding = [&](long long bm, bool thin) {
     const long long tiles = ceil_div((long long)cfg.n, bm), live = (long long)cfg.n - (tiles - 1) * bm;
     const double last = !(thin && thin_enabled()) ? (double)bm
+                        : (live * 8 <= bm && bm == 4 * kThreads) ? bm * 0.21   /* between the forward's 4 and the adjoint's 8 ways */
                         : live * 4 <= bm ? bm * 0.28125 : (live * 2 <= bm ? bm * 0.5625 : (double)bm);
     return ((double)((tiles - 1) * bm) + last) / (double)std::max(cfg.n, (size_t)1) - 1.0;
   };
@@ -287,16 +310,20 @@ LaunchPlan System<T, D>::plan_for(const KernelChoice<T>& k, int n_rows, int row_
   const bool all_rows = row_tiles < 0 || (row_tile0 == 0 && row_tiles == ceil_div(n_rows, p.bm));
   if (thin_on && k.fn_thin != nullptr && all_rows && batch_count == 1 && !comm_active_ && !cluster_combine_ && p.n_row_tiles >= 1) {
     const long long live_last = (long long)n_rows - (long long)(p.n_row_tiles - 1) * p.bm;
-    if (live_last * 4 <= p.bm) p.thin_split = 4;
+    if (live_last * 8 <= p.bm && k.rows_per_thread == 4 && thin8_enabled(MODE)) p.thin_split = 8;  // pair split (pair_kernel)
+    else if (live_last * 4 <= p.bm) p.thin_split = 4;
     else if (live_last * 2 <= p.bm) p.thin_split = 2;
   }
   // A thin tile's units cost a few per cent more than a full tile's (a whole column tile is staged and waited for per
   // 1/thin_split of the work), and stream-K hands every CTA the same number of cells: one cell in `thin_period` of that
   // tile is a phantom, so its CTAs do not finish last (measured).
-  static const int thin_period = [] {
-    const char* e = std::getenv("LMS_THIN_PERIOD");  // experiment knob: 0 = no phantom cells
-    return e ? std::max(std::atoi(e), 0) : 9;
+  static const int thin_period_knob = [] {
+    // experiment knobs: LMS_THIN_PERIOD (all modes) or LMS_THIN_PERIOD_FWD / _ADJ; 0 = no phantom cells, -1 = default
+    const char* e = std::getenv(MODE == kFwd ? "LMS_THIN_PERIOD_FWD" : (MODE == kAdj ? "LMS_THIN_PERIOD_ADJ" : "LMS_THIN_PERIOD_VEL"));
+    if (!e) e = std::getenv("LMS_THIN_PERIOD");
+    return e ? std::max(std::atoi(e), 0) : -1;
   }();
+  const int thin_period = thin_period_knob >= 0 ? thin_period_knob : thin_period_default(MODE, p.thin_split);
   if (p.thin_split > 1 && thin_period > 1) p.thin_period = thin_period;
   const long long thin_units = units_per_row / p.thin_split;
   const long long thin_cells = thin_units + (p.thin_period > 1 ? thin_units / (p.thin_period - 1) : 0);

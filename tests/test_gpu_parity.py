@@ -222,13 +222,14 @@ def test_fp32_shape_variants_agree_with_oracle(hs, oracle, variant, n):
     assert rel_inf(da, oda) <= 1e-5 and rel_inf(db, odb) <= 1e-5
 
 
-@pytest.mark.parametrize("variant,n", [(25, n) for n in (30, 128, 129, 544, 640, 641, 768, 769, 1056, 2180)]
+@pytest.mark.parametrize("variant,n", [(25, n) for n in (30, 64, 65, 128, 129, 544, 576, 577, 640, 641, 768, 769, 1056, 1080, 2180)]
                          + [(0, n) for n in (20, 64, 65, 300, 320, 321, 384, 385, 1100)])
 def test_thin_last_row_tile_agrees_with_oracle(hs, oracle, variant, n):
     """The tiled path's thin last row tile: a last 512-row tile (four-row shapes, variant 25 = the default of large
     problems) or 256-row tile (two-row shapes, variant 0 at these sizes) holding at most a quarter (half) of its rows
     is swept with those rows replicated over 4 (2) groups of warps, each sweeping a quarter (half) of every staged
-    column tile, with phantom cells in the stream-K cell space.  Sizes at and around both thresholds, a single thin
+    column tile, with phantom cells in the stream-K cell space; at most an eighth of a four-row tile (64 rows) is swept
+    8 ways -- the two packed row pairs of a thread hold the same rows and take the two halves of the group's window.  Sizes at and around both thresholds, a single thin
     tile, and thin tiles behind one to four full ones; every entry point that launches the pair kernels, and
     run-to-run bitwise reproducibility."""
     q, p, target, *_ = synth_case(n, 3, 900 + n, spread=7.0)
